@@ -1,0 +1,271 @@
+"""CPU oracle for the UniMGS single-pass rasterizer -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  It wraps
+``oracle/unimgs_oracle.c`` (plain C, see its header for the passages each step
+follows) through ctypes and shares no code with ``paper_2601_19233_b200``.
+
+Parity-unpinned parts: absolute appearance of realistic scenes,
+the triangle sort depth (R9) and per-tile ordering (R8).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "unimgs_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared"]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (no contraction, no fast-math, SSE2 scalar floats)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class CCamera(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("R", C.c_float * 9), ("t", C.c_float * 3),
+                ("near_z", C.c_float), ("far_z", C.c_float)]
+
+
+class CSettings(C.Structure):
+    _fields_ = [("alpha_max", C.c_float), ("t_eps", C.c_float), ("dilation", C.c_float),
+                ("bg", C.c_float * 3), ("bg_alpha", C.c_float)]
+
+
+class CFrag(C.Structure):
+    _fields_ = [("id", C.c_uint32), ("kind", C.c_int32), ("mask", C.c_uint32), ("q", C.c_float),
+                ("depth", C.c_float), ("alpha", C.c_double), ("rgb", C.c_double * 3)]
+
+
+FRAG_DTYPE = np.dtype([("id", np.uint32), ("kind", np.int32), ("mask", np.uint32), ("q", np.float32),
+                       ("depth", np.float32), ("alpha", np.float64), ("rgb", np.float64, (3,))], align=True)
+assert FRAG_DTYPE.itemsize == C.sizeof(CFrag)
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(build())
+        vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+        L.or_create.restype = vp
+        L.or_destroy.argtypes = [vp]
+        L.or_set_scene.argtypes = [vp, i64, vp, vp, vp, vp, vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i32, i32]
+        L.or_project.argtypes = [vp, C.POINTER(CCamera), C.POINTER(CSettings), i32]
+        L.or_project.restype = i32
+        L.or_bin.argtypes = [vp]
+        L.or_bin.restype = i64
+        L.or_render.argtypes = [vp, vp, vp, i64, i32]
+        L.or_render.restype = i32
+        L.or_render_bruteforce.argtypes = [vp, vp, i32]
+        L.or_render_bruteforce.restype = i32
+        L.or_pixel_fragments.argtypes = [vp, i32, i32, vp, i64]
+        L.or_pixel_fragments.restype = i64
+        L.or_support_truncation.argtypes = [vp]
+        L.or_support_truncation.restype = i64
+        L.or_blend_fragments.argtypes = [vp, i32, C.POINTER(CSettings), vp, vp]
+        L.or_blend_fragments.restype = i32
+        L.or_num_pairs.argtypes = [vp]
+        L.or_num_pairs.restype = i64
+        L.or_tiles_x.argtypes = [vp]
+        L.or_tiles_y.argtypes = [vp]
+        L.or_get_gaussian_records.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.or_get_triangle_records.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+        L.or_get_bins.argtypes = [vp, vp, vp, vp]
+        L.or_coverage_mask.argtypes = [vp, i32, i32]
+        L.or_coverage_mask.restype = C.c_uint32
+        L.or_sh_basis_colour.argtypes = [vp, i32, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+def make_settings(alpha_max=0.99, t_eps=1e-4, dilation=0.3, bg=(0.0, 0.0, 0.0), bg_alpha=1.0) -> CSettings:
+    s = CSettings()
+    s.alpha_max, s.t_eps, s.dilation, s.bg_alpha = alpha_max, t_eps, dilation, bg_alpha
+    for i in range(3):
+        s.bg[i] = float(bg[i])
+    return s
+
+
+def make_camera(cam) -> CCamera:
+    c = CCamera()
+    c.width, c.height = cam.width, cam.height
+    c.fx, c.fy, c.cx, c.cy = cam.fx, cam.fy, cam.cx, cam.cy
+    R = np.asarray(cam.R, np.float32).ravel()
+    t = np.asarray(cam.t, np.float32).ravel()
+    for i in range(9):
+        c.R[i] = float(R[i])
+    for i in range(3):
+        c.t[i] = float(t[i])
+    c.near_z, c.far_z = cam.near, cam.far
+    return c
+
+
+def _c(a, dt):
+    return None if a is None else np.ascontiguousarray(a, dt)
+
+
+class Oracle:
+    """One scene, one view at a time.  Arrays are float32/int32/uint8 numpy, borrowed."""
+
+    def __init__(self, gaussians, mesh, threads: int = 0):
+        self.threads = threads
+        L = lib()
+        self._h = L.or_create()
+        g, m = gaussians, mesh
+        self._keep = [
+            _c(g.means, np.float32), _c(g.quats, np.float32), _c(g.scales, np.float32),
+            _c(g.opacities, np.float32), _c(g.sh, np.float32),
+            _c(m.positions, np.float32), _c(m.uvs, np.float32), _c(m.colors, np.float32),
+            _c(m.faces, np.int32), _c(m.opacity, np.float32), _c(m.texture, np.uint8)]
+        k = self._keep
+        tex = m.texture
+        self.N, self.F = int(g.means.shape[0]), int(m.faces.shape[0])
+        L.or_set_scene(self._h, self.N, _ptr(k[0]), _ptr(k[1]), _ptr(k[2]), _ptr(k[3]), _ptr(k[4]),
+                       int(g.sh_degree), int(m.positions.shape[0]), self.F, _ptr(k[5]), _ptr(k[6]),
+                       _ptr(k[7]), _ptr(k[8]), _ptr(k[9]), _ptr(k[10]),
+                       0 if tex is None else int(tex.shape[1]), 0 if tex is None else int(tex.shape[0]))
+        self.cam = None
+
+    def __del__(self):
+        try:
+            lib().or_destroy(self._h)
+        except Exception:
+            pass
+
+    # -- stages --------------------------------------------------------------
+    def project(self, cam, **settings):
+        self.cam = cam
+        self._cs = make_settings(**settings)
+        self._cc = make_camera(cam)
+        rc = lib().or_project(self._h, C.byref(self._cc), C.byref(self._cs), self.threads)
+        if rc:
+            raise MemoryError("oracle projection allocation failed")
+        self.tiles_x = lib().or_tiles_x(self._h)
+        self.tiles_y = lib().or_tiles_y(self._h)
+        return self
+
+    def bin(self) -> int:
+        K = lib().or_bin(self._h)
+        if K < 0:
+            raise MemoryError("oracle binning allocation failed")
+        self.K = int(K)
+        return self.K
+
+    def gaussian_records(self):
+        N = self.N
+        out = dict(rec=np.zeros((N, 8), np.float32), cov=np.zeros((N, 3), np.float32),
+                   rgb=np.zeros((N, 3), np.float64), rect=np.zeros((N, 4), np.int32),
+                   touched=np.zeros(N, np.uint32))
+        lib().or_get_gaussian_records(self._h, _ptr(out["rec"]), _ptr(out["cov"]), _ptr(out["rgb"]),
+                                      _ptr(out["rect"]), _ptr(out["touched"]))
+        return out
+
+    def triangle_records(self):
+        F = self.F
+        out = dict(xy=np.zeros((F, 6), np.int32), vid=np.zeros((F, 3), np.int32), z=np.zeros((F, 3), np.float32),
+                   depth=np.zeros(F, np.float32), rect=np.zeros((F, 4), np.int32), touched=np.zeros(F, np.uint32))
+        lib().or_get_triangle_records(self._h, _ptr(out["xy"]), _ptr(out["vid"]), _ptr(out["z"]),
+                                      _ptr(out["depth"]), _ptr(out["rect"]), _ptr(out["touched"]))
+        return out
+
+    def bins(self):
+        keys = np.zeros(self.K, np.uint64)
+        vals = np.zeros(self.K, np.uint32)
+        ranges = np.zeros((self.tiles_x * self.tiles_y, 2), np.uint32)
+        lib().or_get_bins(self._h, _ptr(keys), _ptr(vals), _ptr(ranges))
+        return keys, vals, ranges
+
+    def render(self, tiles: Optional[Sequence[int]] = None) -> np.ndarray:
+        """Tiled oracle render; pixels of tiles not listed stay NaN."""
+        H, W = self.cam.height, self.cam.width
+        out = np.full((H, W, 4), np.nan, np.float64)
+        tl = None if tiles is None else np.ascontiguousarray(tiles, np.int32)
+        rc = lib().or_render(self._h, _ptr(out), _ptr(tl), 0 if tl is None else len(tl), self.threads)
+        if rc:
+            raise RuntimeError("oracle render before bin()")
+        return out
+
+    def render_bruteforce(self) -> np.ndarray:
+        H, W = self.cam.height, self.cam.width
+        out = np.zeros((H, W, 4), np.float64)
+        lib().or_render_bruteforce(self._h, _ptr(out), self.threads)
+        return out
+
+    def pixel_fragments(self, x: int, y: int) -> np.ndarray:
+        cap = 256
+        while True:
+            buf = np.zeros(cap, FRAG_DTYPE)
+            n = lib().or_pixel_fragments(self._h, x, y, _ptr(buf), cap)
+            if n <= cap:
+                return buf[:n]
+            cap = int(n)
+
+    def support_truncation(self) -> int:
+        return int(lib().or_support_truncation(self._h))
+
+    def full(self, cam, **settings):
+        """project + bin + render: the whole oracle path for one view."""
+        self.project(cam, **settings)
+        self.bin()
+        return self.render()
+
+
+def blend_fragments(frags: np.ndarray, **settings):
+    """Run the unified state machine on an explicit ordered fragment list."""
+    frags = np.ascontiguousarray(frags, FRAG_DTYPE)
+    s = make_settings(**settings)
+    out = np.zeros(4, np.float64)
+    trace = np.zeros(max(len(frags), 1), np.float64)
+    used = lib().or_blend_fragments(_ptr(frags), len(frags), C.byref(s), _ptr(out), _ptr(trace))
+    return out, trace[:used]
+
+
+def frags(*items) -> np.ndarray:
+    """Build a fragment array: items are dicts with kind ('g'|'t'), alpha, rgb, mask, depth, id."""
+    a = np.zeros(len(items), FRAG_DTYPE)
+    for i, it in enumerate(items):
+        a[i]["id"] = it.get("id", i)
+        a[i]["kind"] = 0 if it["kind"] == "g" else 1
+        a[i]["mask"] = it.get("mask", 0)
+        a[i]["alpha"] = it["alpha"]
+        a[i]["rgb"] = it["rgb"]
+        a[i]["depth"] = it.get("depth", float(i + 1))
+    return a
+
+
+def coverage_mask(xy6, x: int, y: int) -> int:
+    xy = np.ascontiguousarray(xy6, np.int32)
+    return int(lib().or_coverage_mask(_ptr(xy), x, y))
+
+
+def sh_colour(coef: np.ndarray, degree: int, direction) -> np.ndarray:
+    coef = np.ascontiguousarray(coef, np.float32)
+    d = np.ascontiguousarray(direction, np.float64)
+    out = np.zeros(3, np.float64)
+    lib().or_sh_basis_colour(_ptr(coef), degree, _ptr(d), _ptr(out))
+    return out
+
+
+def scene_settings(scene, **over):
+    """Default render settings for a synthetic scene (bg from the scene)."""
+    s = dict(alpha_max=0.99, t_eps=1e-4, dilation=0.3, bg=tuple(float(v) for v in scene.bg),
+             bg_alpha=float(scene.bg_alpha))
+    s.update(over)
+    return s
