@@ -1,0 +1,212 @@
+/*
+ * unimgs.h -- C ABI of libunimgs.so, the B200 (sm_100a) implementation of the
+ * UniMGS single-pass anti-aliased mesh + 3DGS tile rasterizer
+ * (arXiv 2601.19233, §3.2).
+ *
+ * The operation: render 3D Gaussians and textured triangle meshes that carry an
+ * opacity attribute ("directly assigning an opacity attribute to textured
+ * meshes allows for unified rendering through alpha-blending") from a
+ * camera in ONE front-to-back alpha-blend.  Gaussian fragments
+ * blend by Eq.1-2; depth-adjacent triangle fragments form an
+ * entity whose transmittance is tracked per sub-pixel sample (Eq.7),
+ * weighted by coverage (Eq.8) and blended by Eq.9; the
+ * background is composited per Eq.10-11.  The readings adopted
+ * where the paper is ambiguous are listed in DESIGN.md §3 (R1-R24).
+ *
+ * The pipeline is three calls per view, enqueued on one CUDA stream:
+ *   unimgs_preprocess  B1 EWA projection of Gaussians + B2 triangle
+ *                      setup with 4-sample coverage (M = 4)
+ *   unimgs_bin         per-tile key duplication, onesweep radix sort and
+ *                      tile ranges ("incorporate triangle fragments into the
+ *                      depth-sorting process")
+ *   unimgs_render      B8 unified blend -> out[H][W][4] = (R, G, B, T)
+ *
+ * Conventions (all calls):
+ *   - Every call returns an unimgs_status; no C++ exception crosses the ABI.
+ *     On failure the context records a message (unimgs_error_string).
+ *   - Array pointers in unimgs_gaussians / unimgs_mesh and the out/debug
+ *     buffers are CUDA DEVICE pointers owned by the caller, except where a
+ *     call says "host".  They must stay valid until the work enqueued on
+ *     `stream` completes.  Host structs are copied at call time.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *   - Host-validated arguments (null required pointers, negative counts,
+ *     counts or sizes above what unimgs_reserve sized, unsupported settings)
+ *     return immediately and enqueue nothing.
+ *   - Device data is NOT validated: NaN, z <= near, non-PD covariance,
+ *     o < 1/255, degenerate or out-of-guard-band triangles are culled as
+ *     values (N1-N7) and counted in unimgs_stats.
+ *   - Capacity: if the number of (tile, primitive) pairs K exceeds the
+ *     reserved max_pairs, nothing is written out of bounds, a device overflow
+ *     flag is set, unimgs_render leaves `out` untouched, and the next
+ *     unimgs_get_stats returns UNIMGS_ERR_CAPACITY with needed_pairs.
+ *   - No call except unimgs_reserve allocates, and no call except
+ *     unimgs_reserve / unimgs_get_stats / unimgs_render_host synchronises the
+ *     host, so preprocess -> bin -> render is CUDA-graph capturable.
+ *   - A context is used by one host thread and one stream at a time.
+ */
+#ifndef UNIMGS_H
+#define UNIMGS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UNIMGS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define UNIMGS_API __attribute__((visibility("default")))
+#else
+#define UNIMGS_API
+#endif
+
+typedef enum {
+    UNIMGS_OK = 0,
+    UNIMGS_ERR_INVALID_ARGUMENT = 1,
+    UNIMGS_ERR_UNSUPPORTED = 2,
+    UNIMGS_ERR_CAPACITY = 3,
+    UNIMGS_ERR_CUDA = 4,
+    UNIMGS_ERR_STATE = 5
+} unimgs_status;
+
+typedef struct unimgs_ctx unimgs_ctx;
+
+/* Pinhole camera (R21): pixel (x, y) covers [x, x+1) x [y, y+1), centre at
+ * (x + .5, y + .5); u = fx * X / Z + cx.  R, t map world to camera, OpenCV
+ * convention (+z forward, y down), R row-major.  near_z default 0.2. */
+typedef struct {
+    int32_t width, height;
+    float fx, fy, cx, cy;
+    float R[9], t[3];
+    float near_z, far_z;
+} unimgs_camera;
+
+/* 3D Gaussians (3DGS parameterisation).  means [N][3], quats [N][4]
+ * (w, x, y, z; need not be normalised), scales [N][3] linear, opacities [N]
+ * post-sigmoid in [0, 1], sh [N][(D+1)^2][3] real SH in the 3DGS basis,
+ * D = sh_degree in 0..3.  count may be 0 (then pointers may be NULL). */
+typedef struct {
+    int64_t count;
+    const float *means, *quats, *scales, *opacities, *sh;
+    int32_t sh_degree;
+} unimgs_gaussians;
+
+/* Triangle mesh with a per-triangle opacity (reading R13).
+ * positions [V][3]; faces [F][3] int32 vertex ids; opacity [F] in [0, 1].
+ * Shading source, first that applies: uvs [V][2] + texture [Ht][Wt][4] RGBA8
+ * (bilinear, texel centres at (i+.5)/W, clamp-to-edge, row 0 at v = 0, alpha
+ * ignored); else colors [V][3]; else white.  num_triangles may be 0. */
+typedef struct {
+    int64_t num_vertices, num_triangles;
+    const float *positions, *uvs, *colors;
+    const int32_t *faces;
+    const float *opacity;
+    const uint8_t *texture;
+    int32_t tex_width, tex_height;
+} unimgs_mesh;
+
+/* Render settings.  Only msaa_samples = 4, tile_size = 16
+ * and alpha_min = 1/255 are supported (else UNIMGS_ERR_UNSUPPORTED).
+ * alpha_max clamps Gaussian alpha; t_eps is the blend-then-test
+ * termination threshold (R16); dilation is added to the cov2d diagonal
+ * (S:194); out = C + T * bg_alpha * bg (Eq.10 under reading R5).
+ * sort_mode: 0 = factored sort (32-bit depth sort of the visible primitives,
+ * then a stable 2-pass radix sort of the pairs by tile), 1 = one onesweep over
+ * 64-bit (tile << 32 | depth) keys.  Both produce the identical order. */
+typedef struct {
+    int32_t msaa_samples, tile_size;
+    float alpha_min, alpha_max, t_eps, dilation;
+    float bg[3], bg_alpha;
+    int32_t sort_mode;
+    int32_t reserved_;
+} unimgs_settings;
+
+typedef struct {
+    int64_t num_pairs;          /* K written (0 on overflow) */
+    int64_t needed_pairs;       /* K required by the last bin */
+    int64_t visible_gaussians;
+    int64_t visible_triangles;
+    int64_t culled_guard_band;  /* triangles culled by near plane / guard band */
+    int32_t overflow;           /* 1 if needed_pairs > reserved max_pairs */
+    int32_t max_tile_pairs;     /* longest tile list */
+    int32_t max_tile_id;        /* its tile index ty * tiles_x + tx */
+    int32_t tiles_x, tiles_y;
+} unimgs_stats;
+
+/* Fill *s with the defaults (M = 4, 16x16 tiles, alpha in [1/255, 0.99],
+ * t_eps 1e-4, dilation 0.3, black opaque background, sort_mode 0). */
+UNIMGS_API void unimgs_default_settings(unimgs_settings *s);
+
+/* Create a context.  s may be NULL (defaults).  No device memory yet. */
+UNIMGS_API int unimgs_create(unimgs_ctx **out, const unimgs_settings *s);
+
+/* Replace the settings (validated as in unimgs_create). */
+UNIMGS_API int unimgs_set_settings(unimgs_ctx *c, const unimgs_settings *s);
+
+/* Allocate all scratch: records for max_prims = N + F primitives, max_pairs
+ * (tile, primitive) pairs, images up to max_w x max_h.  Synchronises the
+ * device.  May be called again to grow. */
+UNIMGS_API int unimgs_reserve(unimgs_ctx *c, int64_t max_prims, int64_t max_pairs, int32_t max_w, int32_t max_h);
+
+/* As unimgs_reserve with separate Gaussian and triangle capacities
+ * (unimgs_reserve(c, P, ...) == unimgs_reserve2(c, P, P, ...)). */
+UNIMGS_API int unimgs_reserve2(unimgs_ctx *c, int64_t max_gaussians, int64_t max_triangles, int64_t max_pairs,
+                    int32_t max_w, int32_t max_h);
+
+/* B1 + B2: project Gaussians (EWA, N1-N5) and set up
+ * triangles (N7).  g or m may be NULL or empty.  Device pointers. */
+UNIMGS_API int unimgs_preprocess(unimgs_ctx *c, const unimgs_gaussians *g, const unimgs_mesh *m,
+                      const unimgs_camera *cam, void *stream);
+
+/* Duplicate (tile, primitive) pairs, sort them by (tile, depth bits, id) and
+ * compute per-tile ranges.  Must follow unimgs_preprocess. */
+UNIMGS_API int unimgs_bin(unimgs_ctx *c, void *stream);
+
+/* B8: the unified single-pass blend (Eq.1-2, 7-11).  Writes
+ * out_rgbt [height][width][4] float32 (R, G, B, final T), device pointer.
+ * Must follow unimgs_bin. */
+UNIMGS_API int unimgs_render(unimgs_ctx *c, float *out_rgbt, void *stream);
+
+/* Synchronise `stream` and report the last frame's counters (host *out). */
+UNIMGS_API int unimgs_get_stats(unimgs_ctx *c, unimgs_stats *out, void *stream);
+
+/* Debug copy of the sorted bins into caller device buffers: keys [K] uint64
+ * (tile << 32 | bits(depth)), vals [K] uint32 unified primitive ids
+ * (triangles 0..F-1, then Gaussians F..F+N-1), ranges [tiles][2] uint32
+ * [start, end).  Any pointer may be NULL.  K from unimgs_get_stats. */
+UNIMGS_API int unimgs_get_bins(unimgs_ctx *c, uint64_t *keys, uint32_t *vals, uint32_t *ranges, void *stream);
+
+/* Debug copy of the per-primitive records into caller device buffers (any
+ * may be NULL):
+ *   grec   [N][12] float: u, v, q_max, o, conic a, b, c, depth, r, g, b, 0
+ *   trec   [F][24] 32-bit words: X0 Y0 X1 Y1 X2 Y2 (int32, 1/256 px, after
+ *          the orientation swap), shading kind, alpha bits, z0 z1 z2 depth,
+ *          then 9 attribute floats, then padding
+ *   rects  [N+F][2] uint32 packed tile rect: x0 | y0 << 16, x1 | y1 << 16
+ *   touched[N+F] uint32 tiles touched (0 = culled), unified id order
+ *   depth_keys [N+F] uint32 bits(depth) (0xFFFFFFFF = culled)            */
+UNIMGS_API int unimgs_get_records(unimgs_ctx *c, float *grec, uint32_t *trec, uint32_t *rects, uint32_t *touched,
+                       uint32_t *depth_keys, void *stream);
+
+/* End-to-end convenience path over HOST buffers: copies the scene (host
+ * arrays in g_host / m_host; pinned memory gives async copies) into
+ * context-owned device buffers, renders n_views cameras, and copies each
+ * frame to out_host [n_views][H][W][4] float32 (all cameras must share one
+ * size).  Synchronises before returning.  Allocates the staging buffers on
+ * first use or growth (so not graph-capturable). */
+UNIMGS_API int unimgs_render_host(unimgs_ctx *c, const unimgs_gaussians *g_host, const unimgs_mesh *m_host,
+                       const unimgs_camera *cams, int32_t n_views, float *out_host, void *stream);
+
+/* Number of kernel launches enqueued by this context since creation. */
+UNIMGS_API int64_t unimgs_launch_count(const unimgs_ctx *c);
+
+/* Last error message of the context (never NULL). */
+UNIMGS_API const char *unimgs_error_string(const unimgs_ctx *c);
+
+UNIMGS_API void unimgs_destroy(unimgs_ctx *c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UNIMGS_H */

@@ -1,0 +1,445 @@
+// api.cu -- the C ABI of libunimgs.so (include/unimgs.h): host-side validation,
+// context / scratch ownership, stream-ordered launches, stats and debug copies.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/unimgs.h"
+#include "internal.cuh"
+
+using namespace unimgs;
+
+struct unimgs_ctx {
+    unimgs_settings set;
+    Buffers buf;
+    int64_t max_g = 0, max_t = 0, max_prims = 0, max_pairs = 0;
+    int max_w = 0, max_h = 0;
+    bool reserved = false;
+    int stage = 0;  // 0 none, 1 preprocessed, 2 binned
+    GaussInput g{};
+    MeshInput m{};
+    CamParams cam{};
+    int64_t P = 0;
+    int sort_mode_used = 0;
+    int sm_count = 148;
+    int64_t launches = 0;
+    std::string err;
+    // end-to-end staging (unimgs_render_host)
+    void *stage_buf = nullptr;
+    size_t stage_bytes = 0;
+    float *frames[2] = {nullptr, nullptr};
+    size_t frame_bytes = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_render[2] = {nullptr, nullptr}, ev_copy[2] = {nullptr, nullptr};
+};
+
+static int fail(unimgs_ctx *c, int code, const char *fmt, ...) __attribute__((format(printf, 3, 4)));
+static int fail(unimgs_ctx *c, int code, const char *fmt, ...) {
+    if (c) {
+        char b[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(b, sizeof b, fmt, ap);
+        va_end(ap);
+        c->err = b;
+    }
+    return code;
+}
+
+#define CUDA_TRY(c, x)                                                                            \
+    do {                                                                                          \
+        cudaError_t e_ = (x);                                                                     \
+        if (e_ != cudaSuccess) return fail(c, UNIMGS_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+    } while (0)
+
+static int check_launch(unimgs_ctx *c, const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, UNIMGS_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+    return UNIMGS_OK;
+}
+
+extern "C" void unimgs_default_settings(unimgs_settings *s) {
+    if (!s) return;
+    memset(s, 0, sizeof *s);
+    s->msaa_samples = 4;
+    s->tile_size = 16;
+    s->alpha_min = 1.0f / 255.0f;
+    s->alpha_max = 0.99f;
+    s->t_eps = 1e-4f;
+    s->dilation = 0.3f;
+    s->bg_alpha = 1.0f;
+    s->sort_mode = 0;
+}
+
+static int validate_settings(unimgs_ctx *c, const unimgs_settings *s) {
+    if (s->msaa_samples != 4) return fail(c, UNIMGS_ERR_UNSUPPORTED, "msaa_samples must be 4 (got %d)", s->msaa_samples);
+    if (s->tile_size != 16) return fail(c, UNIMGS_ERR_UNSUPPORTED, "tile_size must be 16 (got %d)", s->tile_size);
+    if (!(fabs((double)s->alpha_min - 1.0 / 255.0) < 1e-9))
+        return fail(c, UNIMGS_ERR_UNSUPPORTED, "alpha_min must be 1/255 (got %g)", (double)s->alpha_min);
+    if (!(s->alpha_max > 0.f && s->alpha_max <= 1.f)) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "alpha_max not in (0,1]");
+    if (!(s->t_eps >= 0.f && s->t_eps < 1.f)) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "t_eps not in [0,1)");
+    if (!(s->dilation >= 0.f && std::isfinite(s->dilation))) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "dilation < 0");
+    if (s->sort_mode != 0 && s->sort_mode != 1) return fail(c, UNIMGS_ERR_UNSUPPORTED, "sort_mode must be 0 or 1");
+    for (int i = 0; i < 3; i++)
+        if (!std::isfinite(s->bg[i])) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "bg not finite");
+    if (!std::isfinite(s->bg_alpha)) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "bg_alpha not finite");
+    return UNIMGS_OK;
+}
+
+extern "C" int unimgs_create(unimgs_ctx **out, const unimgs_settings *s) {
+    if (!out) return UNIMGS_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    unimgs_ctx *c = new (std::nothrow) unimgs_ctx();
+    if (!c) return UNIMGS_ERR_CUDA;
+    unimgs_default_settings(&c->set);
+    if (s) {
+        int rc = validate_settings(c, s);
+        if (rc) { delete c; return rc; }
+        c->set = *s;
+    }
+    memset(&c->buf, 0, sizeof c->buf);
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0) c->sm_count = n;
+    }
+    *out = c;
+    return UNIMGS_OK;
+}
+
+extern "C" int unimgs_set_settings(unimgs_ctx *c, const unimgs_settings *s) {
+    if (!c || !s) return UNIMGS_ERR_INVALID_ARGUMENT;
+    int rc = validate_settings(c, s);
+    if (rc) return rc;
+    c->set = *s;
+    c->stage = 0;
+    return UNIMGS_OK;
+}
+
+static void free_buffers(unimgs_ctx *c) {
+    Buffers &b = c->buf;
+    void *ptrs[] = {b.rect, b.touched, b.dkey, b.grec, b.trec, b.pk[0], b.pk[1], b.pv[0], b.pv[1], b.tk[0], b.tk[1],
+                    b.tv[0], b.tv[1], b.ranges, b.lookback, b.st};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    memset(&b, 0, sizeof b);
+    c->reserved = false;
+}
+
+extern "C" int unimgs_reserve2(unimgs_ctx *c, int64_t max_gaussians, int64_t max_triangles, int64_t max_pairs,
+                               int32_t max_w, int32_t max_h) {
+    if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (max_gaussians < 0 || max_triangles < 0 || max_pairs < 1 || max_w < 1 || max_h < 1)
+        return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "reserve: bad sizes");
+    if (max_gaussians + max_triangles > 0xFFFFFFFFll)
+        return fail(c, UNIMGS_ERR_UNSUPPORTED, "reserve: more than 2^32-1 primitives");
+    if (max_pairs > (1ll << 30)) return fail(c, UNIMGS_ERR_UNSUPPORTED, "reserve: max_pairs above 2^30");
+    free_buffers(c);
+    Buffers &b = c->buf;
+    const int64_t P = max_gaussians + max_triangles + 1;
+    const int64_t tiles = (int64_t)((max_w + 15) / 16) * ((max_h + 15) / 16);
+    const int64_t lb_tiles = std::max<int64_t>((max_pairs + 4095) / 4096, (P + 2047) / 2048) + 2;
+    CUDA_TRY(c, cudaMalloc(&b.rect, sizeof(uint2) * P));
+    CUDA_TRY(c, cudaMalloc(&b.touched, sizeof(uint32_t) * P));
+    CUDA_TRY(c, cudaMalloc(&b.dkey, sizeof(uint32_t) * P));
+    CUDA_TRY(c, cudaMalloc(&b.grec, sizeof(GaussRecord) * (max_gaussians + 1)));
+    CUDA_TRY(c, cudaMalloc(&b.trec, sizeof(TriRecord) * (max_triangles + 1)));
+    for (int i = 0; i < 2; i++) {
+        CUDA_TRY(c, cudaMalloc(&b.pk[i], sizeof(uint32_t) * P));
+        CUDA_TRY(c, cudaMalloc(&b.pv[i], sizeof(uint32_t) * P));
+        CUDA_TRY(c, cudaMalloc(&b.tk[i], sizeof(uint64_t) * max_pairs));
+        CUDA_TRY(c, cudaMalloc(&b.tv[i], sizeof(uint32_t) * max_pairs));
+    }
+    CUDA_TRY(c, cudaMalloc(&b.ranges, sizeof(uint2) * tiles));
+    CUDA_TRY(c, cudaMalloc(&b.lookback, sizeof(unsigned long long) * 256 * lb_tiles));
+    CUDA_TRY(c, cudaMalloc(&b.st, sizeof(DevState)));
+    CUDA_TRY(c, cudaMemset(b.lookback, 0, sizeof(unsigned long long) * 256 * lb_tiles));
+    CUDA_TRY(c, cudaMemset(b.st, 0, sizeof(DevState)));
+    CUDA_TRY(c, cudaMemset(b.ranges, 0, sizeof(uint2) * tiles));
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    b.max_prims = P - 1;
+    b.max_pairs = max_pairs;
+    b.max_tiles = tiles;
+    b.max_lb_tiles = lb_tiles;
+    b.sorted_vals = b.tv[0];
+    b.sorted_keys = b.tk[0];
+    b.key_bytes = 2;
+    c->max_g = max_gaussians;
+    c->max_t = max_triangles;
+    c->max_prims = P - 1;
+    c->max_pairs = max_pairs;
+    c->max_w = max_w;
+    c->max_h = max_h;
+    c->reserved = true;
+    c->stage = 0;
+    return UNIMGS_OK;
+}
+
+extern "C" int unimgs_reserve(unimgs_ctx *c, int64_t max_prims, int64_t max_pairs, int32_t max_w, int32_t max_h) {
+    return unimgs_reserve2(c, max_prims, max_prims, max_pairs, max_w, max_h);
+}
+
+static int make_cam(unimgs_ctx *c, const unimgs_camera *cam, CamParams &cp) {
+    if (!cam) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "camera is NULL");
+    if (cam->width < 1 || cam->height < 1) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "camera size < 1");
+    if (cam->width > c->max_w || cam->height > c->max_h)
+        return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "camera %dx%d above reserved %dx%d", cam->width, cam->height,
+                    c->max_w, c->max_h);
+    if (!(std::isfinite(cam->fx) && std::isfinite(cam->fy) && cam->fx != 0.f && cam->fy != 0.f))
+        return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "camera focal lengths must be finite and non-zero");
+    cp.W = cam->width;
+    cp.H = cam->height;
+    cp.tiles_x = (cam->width + kTile - 1) / kTile;
+    cp.tiles_y = (cam->height + kTile - 1) / kTile;
+    cp.fx = cam->fx; cp.fy = cam->fy; cp.cx = cam->cx; cp.cy = cam->cy;
+    memcpy(cp.R, cam->R, sizeof cp.R);
+    memcpy(cp.t, cam->t, sizeof cp.t);
+    cp.near_z = cam->near_z;
+    cp.far_z = cam->far_z;
+    for (int a = 0; a < 3; a++)
+        cp.campos[a] = (float)(-((double)cam->R[a] * cam->t[0] + (double)cam->R[3 + a] * cam->t[1] +
+                                 (double)cam->R[6 + a] * cam->t[2]));
+    if ((int64_t)cp.tiles_x * cp.tiles_y > 65536 && c->set.sort_mode == 0)
+        return fail(c, UNIMGS_ERR_UNSUPPORTED, "sort_mode 0 supports at most 65536 tiles; use sort_mode 1");
+    return UNIMGS_OK;
+}
+
+extern "C" int unimgs_preprocess(unimgs_ctx *c, const unimgs_gaussians *g, const unimgs_mesh *m,
+                                 const unimgs_camera *cam, void *stream) {
+    if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (!c->reserved) return fail(c, UNIMGS_ERR_STATE, "preprocess before reserve");
+    CamParams cp;
+    int rc = make_cam(c, cam, cp);
+    if (rc) return rc;
+    GaussInput gi{};
+    if (g && g->count > 0) {
+        if (g->count > c->max_g) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "gaussian count %lld above reserved %lld",
+                                             (long long)g->count, (long long)c->max_g);
+        if (!g->means || !g->quats || !g->scales || !g->opacities || !g->sh)
+            return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "gaussian array is NULL");
+        if (g->sh_degree < 0 || g->sh_degree > 3) return fail(c, UNIMGS_ERR_UNSUPPORTED, "sh_degree must be 0..3");
+        gi = GaussInput{g->count, g->means, g->quats, g->scales, g->opacities, g->sh, g->sh_degree};
+    } else if (g && g->count < 0) {
+        return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "negative gaussian count");
+    }
+    MeshInput mi{};
+    if (m && m->num_triangles > 0) {
+        if (m->num_triangles > c->max_t) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "triangle count above reserved");
+        if (m->num_vertices < 1 || !m->positions || !m->faces || !m->opacity)
+            return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "mesh array is NULL");
+        if (m->texture && (m->tex_width < 1 || m->tex_height < 1))
+            return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "texture size < 1");
+        const uint8_t *tex = (m->texture && m->uvs) ? m->texture : nullptr;
+        mi = MeshInput{m->num_vertices, m->num_triangles, m->positions, m->uvs, m->colors, m->opacity, m->faces,
+                       tex, m->tex_width, m->tex_height};
+    } else if (m && (m->num_triangles < 0 || m->num_vertices < 0)) {
+        return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "negative mesh count");
+    }
+    if (gi.N + mi.F > c->max_prims) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "N + F above reserved");
+    cudaStream_t s = (cudaStream_t)stream;
+    c->launches += launch_begin_frame(c->buf.st, s);
+    c->launches += launch_setup_triangles(mi, cp, c->buf, s);
+    c->launches += launch_preprocess_gaussians(gi, mi.F, cp, c->set.dilation, c->buf, s);
+    rc = check_launch(c, "preprocess");
+    if (rc) return rc;
+    c->g = gi;
+    c->m = mi;
+    c->cam = cp;
+    c->P = gi.N + mi.F;
+    c->stage = 1;
+    return UNIMGS_OK;
+}
+
+extern "C" int unimgs_bin(unimgs_ctx *c, void *stream) {
+    if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (c->stage < 1) return fail(c, UNIMGS_ERR_STATE, "bin before preprocess");
+    c->sort_mode_used = c->set.sort_mode;
+    c->launches += launch_bin(c->buf, c->P, c->g.N, c->m.F, c->cam, c->set.sort_mode, (cudaStream_t)stream, c->sm_count);
+    int rc = check_launch(c, "bin");
+    if (rc) return rc;
+    c->stage = 2;
+    return UNIMGS_OK;
+}
+
+extern "C" int unimgs_render(unimgs_ctx *c, float *out, void *stream) {
+    if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (c->stage < 2) return fail(c, UNIMGS_ERR_STATE, "render before bin");
+    if (!out) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "out is NULL");
+    BlendParams bp{c->set.alpha_max, c->set.t_eps, c->set.bg_alpha, {c->set.bg[0], c->set.bg[1], c->set.bg[2]}};
+    c->launches += launch_blend(c->buf, c->g, c->m, c->cam, bp, out, (cudaStream_t)stream);
+    return check_launch(c, "render");
+}
+
+extern "C" int unimgs_get_stats(unimgs_ctx *c, unimgs_stats *out, void *stream) {
+    if (!c || !out) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (!c->reserved) return fail(c, UNIMGS_ERR_STATE, "stats before reserve");
+    cudaStream_t s = (cudaStream_t)stream;
+    memset(out, 0, sizeof *out);
+    if (c->stage >= 2) {
+        c->launches += launch_tile_stats(c->buf, c->cam.tiles_x * c->cam.tiles_y, s);
+        int rc = check_launch(c, "tile_stats");
+        if (rc) return rc;
+    }
+    DevState h;
+    CUDA_TRY(c, cudaMemcpyAsync(&h, c->buf.st, sizeof h, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    out->num_pairs = h.K;
+    out->needed_pairs = (int64_t)h.needed;
+    out->visible_gaussians = h.vis_g;
+    out->visible_triangles = h.vis_t;
+    out->culled_guard_band = h.culled_guard;
+    out->overflow = (int32_t)h.overflow;
+    out->max_tile_pairs = c->stage >= 2 ? (int32_t)h.max_tile_pairs : 0;
+    out->max_tile_id = c->stage >= 2 ? (int32_t)h.max_tile_id : -1;
+    out->tiles_x = c->cam.tiles_x;
+    out->tiles_y = c->cam.tiles_y;
+    if (h.overflow)
+        return fail(c, UNIMGS_ERR_CAPACITY, "capacity: %llu pairs needed, %lld reserved (heaviest tile %d)",
+                    (unsigned long long)h.needed, (long long)c->max_pairs, out->max_tile_id);
+    return UNIMGS_OK;
+}
+
+extern "C" int unimgs_get_bins(unimgs_ctx *c, uint64_t *keys, uint32_t *vals, uint32_t *ranges, void *stream) {
+    if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (c->stage < 2) return fail(c, UNIMGS_ERR_STATE, "get_bins before bin");
+    cudaStream_t s = (cudaStream_t)stream;
+    DevState h;
+    CUDA_TRY(c, cudaMemcpyAsync(&h, c->buf.st, sizeof h, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (keys) {
+        c->launches += launch_full_keys(c->buf, keys, s);
+        int rc = check_launch(c, "full_keys");
+        if (rc) return rc;
+    }
+    if (vals && h.K) CUDA_TRY(c, cudaMemcpyAsync(vals, c->buf.sorted_vals, sizeof(uint32_t) * h.K, cudaMemcpyDeviceToDevice, s));
+    if (ranges)
+        CUDA_TRY(c, cudaMemcpyAsync(ranges, c->buf.ranges, sizeof(uint2) * c->cam.tiles_x * c->cam.tiles_y,
+                                    cudaMemcpyDeviceToDevice, s));
+    return UNIMGS_OK;
+}
+
+extern "C" int unimgs_get_records(unimgs_ctx *c, float *grec, uint32_t *trec, uint32_t *rects, uint32_t *touched,
+                                  uint32_t *depth_keys, void *stream) {
+    if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (c->stage < 1) return fail(c, UNIMGS_ERR_STATE, "get_records before preprocess");
+    cudaStream_t s = (cudaStream_t)stream;
+    const Buffers &b = c->buf;
+    if (grec && c->g.N) CUDA_TRY(c, cudaMemcpyAsync(grec, b.grec, sizeof(GaussRecord) * c->g.N, cudaMemcpyDeviceToDevice, s));
+    if (trec && c->m.F) CUDA_TRY(c, cudaMemcpyAsync(trec, b.trec, sizeof(TriRecord) * c->m.F, cudaMemcpyDeviceToDevice, s));
+    if (c->P) {
+        if (rects) CUDA_TRY(c, cudaMemcpyAsync(rects, b.rect, sizeof(uint2) * c->P, cudaMemcpyDeviceToDevice, s));
+        if (touched) CUDA_TRY(c, cudaMemcpyAsync(touched, b.touched, sizeof(uint32_t) * c->P, cudaMemcpyDeviceToDevice, s));
+        if (depth_keys) CUDA_TRY(c, cudaMemcpyAsync(depth_keys, b.dkey, sizeof(uint32_t) * c->P, cudaMemcpyDeviceToDevice, s));
+    }
+    return UNIMGS_OK;
+}
+
+// ---- end-to-end path over host buffers ------------------------------------------
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+extern "C" int unimgs_render_host(unimgs_ctx *c, const unimgs_gaussians *gh, const unimgs_mesh *mh,
+                                  const unimgs_camera *cams, int32_t n_views, float *out_host, void *stream) {
+    if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (!c->reserved) return fail(c, UNIMGS_ERR_STATE, "render_host before reserve");
+    if (!cams || n_views < 1 || !out_host) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "render_host: cams/out");
+    const int W = cams[0].width, H = cams[0].height;
+    for (int v = 1; v < n_views; v++)
+        if (cams[v].width != W || cams[v].height != H)
+            return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "render_host: all cameras must share one size");
+    const int64_t N = gh ? gh->count : 0, F = mh ? mh->num_triangles : 0, V = mh ? mh->num_vertices : 0;
+    if (N < 0 || F < 0 || V < 0) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "negative counts");
+    const int shk = N ? (gh->sh_degree + 1) * (gh->sh_degree + 1) : 0;
+    const bool tex = mh && mh->texture && mh->uvs && F;
+    const size_t sz[] = {al256(N * 12), al256(N * 16), al256(N * 12), al256(N * 4), al256(N * shk * 12),
+                         al256(V * 12), al256(mh && mh->uvs ? V * 8 : 0), al256(mh && mh->colors ? V * 12 : 0),
+                         al256(F * 12), al256(F * 4),
+                         al256(tex ? (size_t)mh->tex_width * mh->tex_height * 4 : 0)};
+    size_t total = 0;
+    for (size_t x : sz) total += x;
+    if (total > c->stage_bytes) {
+        if (c->stage_buf) cudaFree(c->stage_buf);
+        c->stage_buf = nullptr;
+        c->stage_bytes = 0;
+        CUDA_TRY(c, cudaMalloc(&c->stage_buf, total));
+        c->stage_bytes = total;
+    }
+    const size_t fb = (size_t)W * H * 16;
+    if (fb > c->frame_bytes) {
+        for (int i = 0; i < 2; i++) {
+            if (c->frames[i]) cudaFree(c->frames[i]);
+            c->frames[i] = nullptr;
+        }
+        c->frame_bytes = 0;
+        for (int i = 0; i < 2; i++) CUDA_TRY(c, cudaMalloc(&c->frames[i], fb));
+        c->frame_bytes = fb;
+    }
+    if (!c->copy_stream) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; i++) {
+            CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_render[i], cudaEventDisableTiming));
+            CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming));
+        }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    char *p = (char *)c->stage_buf;
+    char *dp[11];
+    for (int i = 0; i < 11; i++) { dp[i] = p; p += sz[i]; }
+    const void *src[] = {N ? gh->means : nullptr, N ? gh->quats : nullptr, N ? gh->scales : nullptr,
+                         N ? gh->opacities : nullptr, N ? gh->sh : nullptr, F ? mh->positions : nullptr,
+                         F ? mh->uvs : nullptr, F ? mh->colors : nullptr, F ? mh->faces : nullptr,
+                         F ? mh->opacity : nullptr, tex ? mh->texture : nullptr};
+    const size_t bytes[] = {(size_t)N * 12, (size_t)N * 16, (size_t)N * 12, (size_t)N * 4, (size_t)N * shk * 12,
+                            (size_t)V * 12, (mh && mh->uvs) ? (size_t)V * 8 : 0, (mh && mh->colors) ? (size_t)V * 12 : 0,
+                            (size_t)F * 12, (size_t)F * 4,
+                            tex ? (size_t)mh->tex_width * mh->tex_height * 4 : 0};
+    for (int i = 0; i < 11; i++)
+        if (src[i] && bytes[i]) CUDA_TRY(c, cudaMemcpyAsync(dp[i], src[i], bytes[i], cudaMemcpyHostToDevice, s));
+    unimgs_gaussians gd{N, (const float *)dp[0], (const float *)dp[1], (const float *)dp[2], (const float *)dp[3],
+                        (const float *)dp[4], N ? gh->sh_degree : 0};
+    unimgs_mesh md{V, F, (const float *)dp[5], (F && mh->uvs) ? (const float *)dp[6] : nullptr,
+                   (F && mh->colors) ? (const float *)dp[7] : nullptr, (const int32_t *)dp[8], (const float *)dp[9],
+                   tex ? (const uint8_t *)dp[10] : nullptr, tex ? mh->tex_width : 0, tex ? mh->tex_height : 0};
+    for (int v = 0; v < n_views; v++) {
+        const int bi = v & 1;
+        if (v >= 2) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_copy[bi], 0));
+        int rc = unimgs_preprocess(c, &gd, &md, &cams[v], stream);
+        if (!rc) rc = unimgs_bin(c, stream);
+        if (!rc) rc = unimgs_render(c, c->frames[bi], stream);
+        if (rc) return rc;
+        CUDA_TRY(c, cudaEventRecord(c->ev_render[bi], s));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_render[bi], 0));
+        CUDA_TRY(c, cudaMemcpyAsync(out_host + (size_t)v * W * H * 4, c->frames[bi], fb, cudaMemcpyDeviceToHost,
+                                    c->copy_stream));
+        CUDA_TRY(c, cudaEventRecord(c->ev_copy[bi], c->copy_stream));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->copy_stream));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    DevState h;
+    CUDA_TRY(c, cudaMemcpy(&h, c->buf.st, sizeof h, cudaMemcpyDeviceToHost));
+    if (h.overflow) return fail(c, UNIMGS_ERR_CAPACITY, "capacity: %llu pairs needed", (unsigned long long)h.needed);
+    return UNIMGS_OK;
+}
+
+extern "C" int64_t unimgs_launch_count(const unimgs_ctx *c) { return c ? c->launches : 0; }
+
+extern "C" const char *unimgs_error_string(const unimgs_ctx *c) {
+    if (!c) return "null context";
+    return c->err.empty() ? "ok" : c->err.c_str();
+}
+
+extern "C" void unimgs_destroy(unimgs_ctx *c) {
+    if (!c) return;
+    free_buffers(c);
+    if (c->stage_buf) cudaFree(c->stage_buf);
+    for (int i = 0; i < 2; i++) {
+        if (c->frames[i]) cudaFree(c->frames[i]);
+        if (c->ev_render[i]) cudaEventDestroy(c->ev_render[i]);
+        if (c->ev_copy[i]) cudaEventDestroy(c->ev_copy[i]);
+    }
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    delete c;
+}

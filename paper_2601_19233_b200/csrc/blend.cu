@@ -1,0 +1,206 @@
+// blend.cu -- B8: the unified single-pass anti-aliased blend (§3.2).
+//
+// One CTA per 16x16 tile, one thread per pixel.  The tile's sorted list
+// (unified ids, (tile, depth, id) order) is staged through shared memory in
+// batches of 256 entries; Gaussian records are gathered with 16-byte loads
+// into SoA shared arrays, triangle entries are resolved from their 96-byte
+// setup record (broadcast loads: every lane reads the same address).
+//
+// Per pixel (state machine of DESIGN.md §2 / the oracle):
+//   Gaussian fragment  iff q <= q_max (N6, bit-exact with the oracle):
+//       close an open entity (T = T_e * mean_j t_j, reading R3),
+//       alpha = min(alpha_max, o e^{-q/2}); C += T alpha c; T *= 1 - alpha  (Eq.1-2)
+//   triangle fragment  iff its 4-sample coverage mask m != 0 (exact int64
+//       edge functions, top-left rule, D3D 4x pattern; N7, R10-R11):
+//       open an entity if none (T_e = T, t_j = 1; Eq.7), O = sum_j m_j t_j / 4
+//       (Eq.8), C += T_e O alpha c (Eq.9), t_j *= 1 - m_j alpha (Eq.7)
+//   stop once T_eff < t_eps (blend-then-test, R16); the block exits when
+//   every pixel has stopped (__syncthreads_count).
+//   out = (C + T bg_alpha bg, T) with the exit T of an open entity (R3, R5).
+// Triangle colour: perspective-correct barycentrics at the pixel centre in
+// fp64 (lambda_k ~ E_k z_i z_j, exact products), manual fp32 bilinear texture.
+#include "internal.cuh"
+
+namespace unimgs {
+
+struct TexView {
+    const uchar4 *tex;
+    int w, h;
+};
+
+__device__ __forceinline__ float4 texel(const TexView &t, int i, int j) {
+    i = min(max(i, 0), t.w - 1);
+    j = min(max(j, 0), t.h - 1);
+    const uchar4 c = __ldg(t.tex + (size_t)j * t.w + i);
+    return make_float4(c.x, c.y, c.z, c.w);
+}
+
+// 4x coverage mask of a triangle record at pixel (x, y): sample j at
+// (256x + 128 + 16 ox_j, 256y + 128 + 16 oy_j), offsets (-2,-6) (6,-2) (-6,2) (2,6).
+__device__ __forceinline__ unsigned coverage(const int X[3], const int Y[3], int x, int y, long long Ec[3]) {
+    const int PX = 256 * x + 128, PY = 256 * y + 128;
+    unsigned m = 0xF;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        const int a = (k + 1) % 3, b = (k + 2) % 3;
+        const int dx = X[b] - X[a], dy = Y[b] - Y[a];
+        // E_k(P) = dx (PY - Ya) - dy (PX - Xa) at the centre, then per-sample offsets
+        const long long e = (long long)dx * (PY - Y[a]) - (long long)dy * (PX - X[a]);
+        Ec[k] = e;
+        const long long thr = (dy > 0 || (dy == 0 && dx < 0)) ? 0 : 1;
+        // sample offsets (in 1/256 px): 16 * (dx * oy - dy * ox)
+        const long long e0 = e + 16LL * ((long long)dx * -6 - (long long)dy * -2);
+        const long long e1 = e + 16LL * ((long long)dx * -2 - (long long)dy * 6);
+        const long long e2 = e + 16LL * ((long long)dx * 2 - (long long)dy * -6);
+        const long long e3 = e + 16LL * ((long long)dx * 6 - (long long)dy * 2);
+        unsigned mk = (e0 >= thr ? 1u : 0u) | (e1 >= thr ? 2u : 0u) | (e2 >= thr ? 4u : 0u) | (e3 >= thr ? 8u : 0u);
+        m &= mk;
+    }
+    return m;
+}
+
+__device__ __forceinline__ void tri_colour(const TriRecord &r, const long long Ec[3], const TexView &tv, float rgb[3]) {
+    const double z0 = r.q2.x, z1 = r.q2.y, z2 = r.q2.z;
+    // w_k = b_k / z_k  ~  E_k * (product of the other two z): exact products in fp64
+    const double w0 = (double)Ec[0] * (z1 * z2), w1 = (double)Ec[1] * (z0 * z2), w2 = (double)Ec[2] * (z0 * z1);
+    const double sw = w0 + w1 + w2;
+    double l0, l1, l2;
+    if (sw != 0.0) {
+        const double is = 1.0 / sw;
+        l0 = w0 * is; l1 = w1 * is; l2 = w2 * is;
+    } else {
+        const double A2 = (double)(Ec[0] + Ec[1] + Ec[2]);
+        l0 = Ec[0] / A2; l1 = Ec[1] / A2; l2 = Ec[2] / A2;
+    }
+    const int kind = r.q1.z;
+    if (kind == 1) {
+        const double uu = l0 * r.q3.x + l1 * r.q3.w + l2 * r.q4.z;
+        const double vv = l0 * r.q3.y + l1 * r.q4.x + l2 * r.q4.w;
+        const double txd = uu * tv.w - 0.5, tyd = vv * tv.h - 0.5;
+        const double fi = floor(txd), fj = floor(tyd);
+        const float ax = (float)(txd - fi), ay = (float)(tyd - fj);
+        // clamp before converting so huge coordinates stay defined
+        const int i0 = (int)fmin(fmax(fi, -2.0), (double)tv.w + 1.0);
+        const int j0 = (int)fmin(fmax(fj, -2.0), (double)tv.h + 1.0);
+        const float4 t00 = texel(tv, i0, j0), t10 = texel(tv, i0 + 1, j0);
+        const float4 t01 = texel(tv, i0, j0 + 1), t11 = texel(tv, i0 + 1, j0 + 1);
+        const float s = 1.0f / 255.0f;
+        rgb[0] = ((1.f - ay) * ((1.f - ax) * t00.x + ax * t10.x) + ay * ((1.f - ax) * t01.x + ax * t11.x)) * s;
+        rgb[1] = ((1.f - ay) * ((1.f - ax) * t00.y + ax * t10.y) + ay * ((1.f - ax) * t01.y + ax * t11.y)) * s;
+        rgb[2] = ((1.f - ay) * ((1.f - ax) * t00.z + ax * t10.z) + ay * ((1.f - ax) * t01.z + ax * t11.z)) * s;
+    } else if (kind == 0) {
+        const double c0 = l0 * r.q3.x + l1 * r.q3.w + l2 * r.q4.z;
+        const double c1 = l0 * r.q3.y + l1 * r.q4.x + l2 * r.q4.w;
+        const double c2 = l0 * r.q3.z + l1 * r.q4.y + l2 * r.q5.x;
+        rgb[0] = (float)fmin(fmax(c0, 0.0), 1.0);
+        rgb[1] = (float)fmin(fmax(c1, 0.0), 1.0);
+        rgb[2] = (float)fmin(fmax(c2, 0.0), 1.0);
+    } else {
+        rgb[0] = rgb[1] = rgb[2] = 1.f;
+    }
+}
+
+__global__ void __launch_bounds__(kBlendThreads) k_blend(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ vals,
+                                                         const GaussRecord *__restrict__ grec,
+                                                         const TriRecord *__restrict__ trec, TexView tv, unsigned F,
+                                                         int W, int H, int tiles_x, BlendParams bp,
+                                                         float4 *__restrict__ out, const DevState *st) {
+    if (st->overflow) return;
+    __shared__ float4 s_a[kBlendThreads];  // u, v, q_max, o
+    __shared__ float4 s_b[kBlendThreads];  // ca, 2 cb, cc, -
+    __shared__ float4 s_c[kBlendThreads];  // r, g, b, -
+    __shared__ unsigned s_id[kBlendThreads];
+
+    const int tile = blockIdx.x;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
+    const bool inside = x < W && y < H;
+    const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+    const uint2 rg = ranges[tile];
+
+    float C0 = 0.f, C1 = 0.f, C2 = 0.f, T = 1.f, Te = 1.f;
+    float t0 = 1.f, t1 = 1.f, t2 = 1.f, t3 = 1.f;
+    bool open = false, done = !inside;
+
+    for (unsigned base = rg.x; base < rg.y; base += kBlendThreads) {
+        if (__syncthreads_count(done) == kBlendThreads) break;
+        const unsigned i = base + threadIdx.x;
+        if (i < rg.y) {
+            const unsigned id = __ldg(vals + i);
+            s_id[threadIdx.x] = id;
+            if (id >= F) {
+                const GaussRecord *g = grec + (id - F);
+                const float4 a = __ldg(&g->a), bb = __ldg(&g->b), c = __ldg(&g->c);
+                s_a[threadIdx.x] = a;
+                s_b[threadIdx.x] = make_float4(bb.x, bb.y + bb.y, bb.z, 0.f);
+                s_c[threadIdx.x] = c;
+            }
+        }
+        __syncthreads();
+        if (done) continue;
+        const unsigned n = min((unsigned)kBlendThreads, rg.y - base);
+        for (unsigned j = 0; j < n; j++) {
+            const unsigned id = s_id[j];
+            if (id >= F) {
+                const float4 a = s_a[j];
+                const float dx = __fsub_rn(px, a.x), dy = __fsub_rn(py, a.y);
+                const float4 b = s_b[j];
+                const float q = __fmaf_rn(b.x, __fmul_rn(dx, dx), __fmaf_rn(b.z, __fmul_rn(dy, dy), __fmul_rn(b.y, __fmul_rn(dx, dy))));
+                if (!(q <= a.z)) continue;
+                const float al = fminf(bp.alpha_max, a.w * __expf(-0.5f * q));
+                if (open) {
+                    T = Te * ((t0 + t1) + (t2 + t3)) * 0.25f;
+                    open = false;
+                }
+                const float4 c = s_c[j];
+                const float w = T * al;
+                C0 += w * c.x; C1 += w * c.y; C2 += w * c.z;
+                T -= w;
+                if (T < bp.t_eps) { done = true; break; }
+            } else {
+                const TriRecord &r = trec[id];
+                const int4 q0 = r.q0, q1 = r.q1;
+                const int X[3] = {q0.x, q0.z, q1.x}, Y[3] = {q0.y, q0.w, q1.y};
+                long long Ec[3];
+                const unsigned m = coverage(X, Y, x, y, Ec);
+                if (!m) continue;
+                TriRecord rr;
+                rr.q0 = q0; rr.q1 = q1; rr.q2 = r.q2; rr.q3 = r.q3; rr.q4 = r.q4; rr.q5 = r.q5;
+                float rgb[3];
+                tri_colour(rr, Ec, tv, rgb);
+                const float al = __int_as_float(q1.w);
+                if (!open) {
+                    open = true;
+                    Te = T;
+                    t0 = t1 = t2 = t3 = 1.f;
+                }
+                const float O = (((m & 1) ? t0 : 0.f) + ((m & 2) ? t1 : 0.f) + ((m & 4) ? t2 : 0.f) + ((m & 8) ? t3 : 0.f)) * 0.25f;
+                const float w = Te * O * al;
+                C0 += w * rgb[0]; C1 += w * rgb[1]; C2 += w * rgb[2];
+                const float k = 1.f - al;
+                if (m & 1) t0 *= k;
+                if (m & 2) t1 *= k;
+                if (m & 4) t2 *= k;
+                if (m & 8) t3 *= k;
+                if (Te * ((t0 + t1) + (t2 + t3)) * 0.25f < bp.t_eps) { done = true; break; }
+            }
+        }
+    }
+    if (open) T = Te * ((t0 + t1) + (t2 + t3)) * 0.25f;
+    if (inside) {
+        const float s = T * bp.bg_alpha;
+        out[(size_t)y * W + x] = make_float4(C0 + s * bp.bg[0], C1 + s * bp.bg[1], C2 + s * bp.bg[2], T);
+    }
+}
+
+int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, const CamParams &cam,
+                 const BlendParams &bp, float *out, cudaStream_t s) {
+    (void)g;
+    const int tiles = cam.tiles_x * cam.tiles_y;
+    TexView tv{reinterpret_cast<const uchar4 *>(m.tex), m.tw, m.th};
+    k_blend<<<tiles, kBlendThreads, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv, (unsigned)m.F, cam.W, cam.H,
+                                            cam.tiles_x, bp, reinterpret_cast<float4 *>(out), b.st);
+    return 1;
+}
+
+}  // namespace unimgs

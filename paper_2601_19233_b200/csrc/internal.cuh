@@ -1,0 +1,108 @@
+// internal.cuh -- device-side data layout and launch interface of libunimgs.
+// Shared by the .cu files of the CUDA path only (never by oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace unimgs {
+
+constexpr int kTile = 16;
+constexpr int kBlendThreads = 256;
+constexpr int kMaxPasses = 8;
+
+// Per-frame device counters.  frame_epoch survives across frames (it tags
+// decoupled-look-back entries so the look-back buffers never need clearing);
+// everything after it is zeroed by k_begin_frame.
+struct DevState {
+    unsigned int frame_epoch;
+    unsigned int pad0;
+    unsigned int n_vis;         // visible primitives (compacted)
+    unsigned int K;             // pairs written (0 on overflow)
+    unsigned long long needed;  // pairs required (saturating at 2^32-1)
+    unsigned int overflow;
+    unsigned int vis_g, vis_t, culled_guard;
+    unsigned int ctr[16];       // dynamic tile counters of the scans / sort passes
+    unsigned int hist[kMaxPasses][256];
+    unsigned int max_tile_pairs, max_tile_id;
+};
+
+// Camera + the per-frame constants every stage needs.
+struct CamParams {
+    int W, H, tiles_x, tiles_y;
+    float fx, fy, cx, cy;
+    float R[9], t[3];
+    float near_z, far_z;
+    float campos[3];
+};
+
+// Triangle record, 96 B (6 x 16 B), written by B2 and read by B8:
+//   q0 int4   {X0, Y0, X1, Y1}          snapped 1/256-px coords after orientation
+//   q1 int4   {X2, Y2, kind, alpha bits} kind 1 = textured (uv), 0 = vertex colours, 2 = white
+//   q2 float4 {z0, z1, z2, depth}       view z per vertex; sort depth
+//   q3 float4 {a0.x, a0.y, a0.z, a1.x}  shading attributes per vertex (uv,0 or rgb)
+//   q4 float4 {a1.y, a1.z, a2.x, a2.y}
+//   q5 float4 {a2.z, 0, 0, 0}
+struct TriRecord {
+    int4 q0, q1;
+    float4 q2, q3, q4, q5;
+};
+
+// Gaussian record, 48 B: {u, v, q_max, o}, {ca, cb, cc, depth}, {r, g, b, 0}.
+struct GaussRecord {
+    float4 a, b, c;
+};
+
+struct Buffers {
+    // per primitive, unified id (triangles 0..F-1, Gaussians F..F+N-1)
+    uint2 *rect;          // x0 | y0 << 16, x1 | y1 << 16
+    uint32_t *touched;
+    uint32_t *dkey;       // bits(depth), 0xFFFFFFFF if culled
+    GaussRecord *grec;    // [N]
+    TriRecord *trec;      // [F]
+    // sort buffers
+    uint32_t *pk[2];      // depth keys ping-pong [max_prims]
+    uint32_t *pv[2];      // primitive ids ping-pong [max_prims]
+    void *tk[2];          // pair keys ping-pong (uint16 tile ids, or uint64 full keys) [max_pairs]
+    uint32_t *tv[2];      // pair values ping-pong [max_pairs]
+    uint2 *ranges;        // [tiles]
+    unsigned long long *lookback;  // [max_lb_tiles][256]
+    DevState *st;
+    int64_t max_prims, max_pairs, max_tiles, max_lb_tiles;
+    const uint32_t *sorted_vals;   // final per-tile lists (points into tv[*])
+    const void *sorted_keys;       // final keys (tk[*])
+    int key_bytes;                 // 2 (factored) or 8 (full)
+};
+
+struct GaussInput {
+    int64_t N;
+    const float *means, *quats, *scales, *opac, *sh;
+    int sh_degree;
+};
+
+struct MeshInput {
+    int64_t V, F;
+    const float *pos, *uvs, *cols, *opac;
+    const int32_t *faces;
+    const uint8_t *tex;
+    int tw, th;
+};
+
+struct BlendParams {
+    float alpha_max, t_eps, bg_alpha;
+    float bg[3];
+};
+
+// ---- launchers (return number of kernels enqueued) --------------------------
+int launch_begin_frame(DevState *st, cudaStream_t s);
+int launch_preprocess_gaussians(const GaussInput &g, int64_t F, const CamParams &cam, float dilation,
+                                const Buffers &b, cudaStream_t s);
+int launch_setup_triangles(const MeshInput &m, const CamParams &cam, const Buffers &b, cudaStream_t s);
+// binning: factored (sort_mode 0) or full 64-bit keys (sort_mode 1)
+int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam, int sort_mode, cudaStream_t s,
+               int sm_count);
+int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, const CamParams &cam,
+                 const BlendParams &bp, float *out, cudaStream_t s);
+int launch_tile_stats(const Buffers &b, int tiles, cudaStream_t s);
+int launch_full_keys(const Buffers &b, uint64_t *keys, cudaStream_t s);
+
+}  // namespace unimgs

@@ -1,0 +1,247 @@
+"""Thin Python binding over the C ABI (include/unimgs.h).
+
+PyTorch supplies device memory and the stream; every step of the path runs in
+libunimgs.so's kernels.  No CPU fallback exists: a missing library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .scenes import Camera as SceneCamera
+
+
+@dataclass
+class DeviceScene:
+    """Scene arrays resident in device memory (torch tensors)."""
+    means: torch.Tensor
+    quats: torch.Tensor
+    scales: torch.Tensor
+    opacities: torch.Tensor
+    sh: torch.Tensor
+    sh_degree: int
+    positions: torch.Tensor
+    faces: torch.Tensor
+    opacity: torch.Tensor
+    uvs: Optional[torch.Tensor] = None
+    colors: Optional[torch.Tensor] = None
+    texture: Optional[torch.Tensor] = None
+
+    @property
+    def num_gaussians(self) -> int:
+        return int(self.means.shape[0])
+
+    @property
+    def num_triangles(self) -> int:
+        return int(self.faces.shape[0])
+
+    def nbytes(self) -> int:
+        ts = [self.means, self.quats, self.scales, self.opacities, self.sh, self.positions, self.faces,
+              self.opacity, self.uvs, self.colors, self.texture]
+        return int(sum(t.numel() * t.element_size() for t in ts if t is not None))
+
+
+def to_device(scene, device="cuda") -> DeviceScene:
+    g, m = scene.gaussians, scene.mesh
+
+    def t(a):
+        return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(device)
+
+    return DeviceScene(t(g.means), t(g.quats), t(g.scales), t(g.opacities), t(g.sh), int(g.sh_degree),
+                       t(m.positions), t(m.faces.astype(np.int32)), t(m.opacity), t(m.uvs), t(m.colors), t(m.texture))
+
+
+def to_pinned(scene) -> DeviceScene:
+    """Host copies in page-locked memory (inputs of the end-to-end path)."""
+    ds = to_device(scene, "cpu")
+    for k, v in list(ds.__dict__.items()):
+        if isinstance(v, torch.Tensor):
+            setattr(ds, k, v.pin_memory())
+    return ds
+
+
+def c_camera(cam: SceneCamera) -> _lib.Camera:
+    c = _lib.Camera()
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    R = np.asarray(cam.R, np.float32).ravel()
+    t = np.asarray(cam.t, np.float32).ravel()
+    for i in range(9):
+        c.R[i] = float(R[i])
+    for i in range(3):
+        c.t[i] = float(t[i])
+    c.near_z, c.far_z = float(cam.near), float(cam.far)
+    return c
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    assert t.is_contiguous()
+    return t.data_ptr()
+
+
+def c_gaussians(s: DeviceScene) -> _lib.Gaussians:
+    g = _lib.Gaussians()
+    g.count = s.num_gaussians
+    g.means, g.quats, g.scales = _ptr(s.means), _ptr(s.quats), _ptr(s.scales)
+    g.opacities, g.sh, g.sh_degree = _ptr(s.opacities), _ptr(s.sh), int(s.sh_degree)
+    return g
+
+
+def c_mesh(s: DeviceScene) -> _lib.Mesh:
+    m = _lib.Mesh()
+    m.num_vertices, m.num_triangles = int(s.positions.shape[0]), s.num_triangles
+    m.positions, m.uvs, m.colors = _ptr(s.positions), _ptr(s.uvs), _ptr(s.colors)
+    m.faces, m.opacity, m.texture = _ptr(s.faces), _ptr(s.opacity), _ptr(s.texture)
+    if s.texture is not None:
+        m.tex_height, m.tex_width = int(s.texture.shape[0]), int(s.texture.shape[1])
+    return m
+
+
+def make_settings(alpha_max=0.99, t_eps=1e-4, dilation=0.3, bg=(0.0, 0.0, 0.0), bg_alpha=1.0,
+                  sort_mode=0) -> _lib.Settings:
+    s = _lib.Settings()
+    _lib.load().unimgs_default_settings(C.byref(s))
+    s.alpha_max, s.t_eps, s.dilation, s.bg_alpha, s.sort_mode = alpha_max, t_eps, dilation, bg_alpha, sort_mode
+    for i in range(3):
+        s.bg[i] = float(bg[i])
+    return s
+
+
+def _stream_handle(stream: Optional[torch.cuda.Stream]):
+    st = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(st.cuda_stream)
+
+
+class Renderer:
+    """One unimgs context: reserve once, then preprocess -> bin -> render per view."""
+
+    def __init__(self, max_gaussians: int, max_triangles: int, max_pairs: int, max_w: int, max_h: int, **settings):
+        self.L = _lib.load()
+        self._h = C.c_void_p()
+        self._settings = make_settings(**settings)
+        self._check(self.L.unimgs_create(C.byref(self._h), C.byref(self._settings)), create=True)
+        self._check(self.L.unimgs_reserve2(self._h, max_gaussians, max_triangles, max_pairs, max_w, max_h))
+        self.max_w, self.max_h = max_w, max_h
+        self._cam = None
+        self._scene = None
+
+    def _check(self, rc: int, create: bool = False):
+        if rc != _lib.OK:
+            msg = "create failed" if create else self.L.unimgs_error_string(self._h).decode()
+            raise _lib.UnimgsError(rc, msg)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self.L.unimgs_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_settings(self, **settings):
+        self._settings = make_settings(**settings)
+        self._check(self.L.unimgs_set_settings(self._h, C.byref(self._settings)))
+
+    # ---- the three calls -------------------------------------------------
+    def preprocess(self, scene: DeviceScene, cam: SceneCamera, stream=None):
+        self._g, self._m, self._cam_c = c_gaussians(scene), c_mesh(scene), c_camera(cam)
+        self._cam, self._scene = cam, scene
+        self._check(self.L.unimgs_preprocess(self._h, C.byref(self._g), C.byref(self._m), C.byref(self._cam_c),
+                                             _stream_handle(stream)))
+
+    def bin(self, stream=None):
+        self._check(self.L.unimgs_bin(self._h, _stream_handle(stream)))
+
+    def render(self, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((self._cam.height, self._cam.width, 4), dtype=torch.float32, device="cuda")
+        assert out.is_cuda and out.dtype == torch.float32 and out.is_contiguous()
+        self._check(self.L.unimgs_render(self._h, C.c_void_p(out.data_ptr()), _stream_handle(stream)))
+        return out
+
+    def render_view(self, scene: DeviceScene, cam: SceneCamera, out=None, stream=None) -> torch.Tensor:
+        self.preprocess(scene, cam, stream)
+        self.bin(stream)
+        return self.render(out, stream)
+
+    # ---- host-buffer end-to-end path ---------------------------------------
+    def render_host(self, host_scene: DeviceScene, cams: Sequence[SceneCamera], out: torch.Tensor, stream=None):
+        """host_scene tensors on the CPU (pinned for async copies); out: pinned CPU [V,H,W,4] float32."""
+        g, m = c_gaussians(host_scene), c_mesh(host_scene)
+        arr = (_lib.Camera * len(cams))(*[c_camera(c) for c in cams])
+        assert not out.is_cuda and out.is_contiguous()
+        self._check(self.L.unimgs_render_host(self._h, C.byref(g), C.byref(m), arr, len(cams),
+                                              C.c_void_p(out.data_ptr()), _stream_handle(stream)))
+        return out
+
+    # ---- stats / debug --------------------------------------------------------
+    def stats(self, stream=None, check: bool = True) -> dict:
+        st = _lib.Stats()
+        rc = self.L.unimgs_get_stats(self._h, C.byref(st), _stream_handle(stream))
+        if check:
+            self._check(rc)
+        d = {k: getattr(st, k) for k, _ in _lib.Stats._fields_}
+        d["status"] = rc
+        return d
+
+    def bins(self, stream=None):
+        st = self.stats(stream)
+        K = st["num_pairs"]
+        tiles = st["tiles_x"] * st["tiles_y"]
+        keys = torch.empty(max(K, 1), dtype=torch.int64, device="cuda")
+        vals = torch.empty(max(K, 1), dtype=torch.int32, device="cuda")
+        ranges = torch.empty((tiles, 2), dtype=torch.int32, device="cuda")
+        self._check(self.L.unimgs_get_bins(self._h, C.c_void_p(keys.data_ptr()), C.c_void_p(vals.data_ptr()),
+                                           C.c_void_p(ranges.data_ptr()), _stream_handle(stream)))
+        torch.cuda.synchronize()
+        k = keys[:K].cpu().numpy().view(np.uint64)
+        v = vals[:K].cpu().numpy().view(np.uint32)
+        r = ranges.cpu().numpy().view(np.uint32)
+        return k, v, r
+
+    def records(self, stream=None) -> dict:
+        s = self._scene
+        N, F = s.num_gaussians, s.num_triangles
+        P = N + F
+        grec = torch.empty((max(N, 1), 12), dtype=torch.float32, device="cuda")
+        trec = torch.empty((max(F, 1), 24), dtype=torch.int32, device="cuda")
+        rects = torch.empty((max(P, 1), 2), dtype=torch.int32, device="cuda")
+        touched = torch.empty(max(P, 1), dtype=torch.int32, device="cuda")
+        dkeys = torch.empty(max(P, 1), dtype=torch.int32, device="cuda")
+        self._check(self.L.unimgs_get_records(self._h, C.c_void_p(grec.data_ptr()), C.c_void_p(trec.data_ptr()),
+                                              C.c_void_p(rects.data_ptr()), C.c_void_p(touched.data_ptr()),
+                                              C.c_void_p(dkeys.data_ptr()), _stream_handle(stream)))
+        torch.cuda.synchronize()
+        rect = rects[:P].cpu().numpy().view(np.uint32)
+        unpacked = np.stack([rect[:, 0] & 0xFFFF, rect[:, 0] >> 16, rect[:, 1] & 0xFFFF, rect[:, 1] >> 16], -1)
+        return dict(grec=grec[:N].cpu().numpy(), trec=trec[:F].cpu().numpy(),
+                    rect=unpacked.astype(np.int32), touched=touched[:P].cpu().numpy().view(np.uint32),
+                    dkey=dkeys[:P].cpu().numpy().view(np.uint32))
+
+    def launch_count(self) -> int:
+        return int(self.L.unimgs_launch_count(self._h))
+
+
+def estimate_pairs(scene, slack: float = 2.0, minimum: int = 1 << 16) -> int:
+    """A generous max_pairs for a scene (the caller may also size from get_stats)."""
+    n = scene.gaussians.count + scene.mesh.num_triangles
+    return int(max(minimum, n * 4 * slack))
+
+
+def renderer_for(scene, max_pairs: Optional[int] = None, **settings) -> Renderer:
+    W = max(c.width for c in scene.cameras)
+    H = max(c.height for c in scene.cameras)
+    settings.setdefault("bg", tuple(float(v) for v in scene.bg))
+    settings.setdefault("bg_alpha", float(scene.bg_alpha))
+    return Renderer(max(scene.gaussians.count, 1), max(scene.mesh.num_triangles, 1),
+                    max_pairs or estimate_pairs(scene), W, H, **settings)
