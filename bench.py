@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark: 1080p unified mesh+3DGS render frames/s on N B200s (BASELINE.json metric).
+
+Workload (BASELINE.json configs[4], "multi-view batch"): the mip360-like scene
+(3M Gaussians, SH degree 3, + 200k textured triangles), cameras from the
+256-view 1080p orbit.  One step = every rank renders `--views` views of the
+orbit (view i -> rank i mod N) through preprocess -> bin -> render, and ranks
+r > 0 send their frames to rank 0 over NCCL (the only collective).
+Per-GPU work is fixed as N grows ("scaling": "weak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--views V] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Rank 0 prints one JSON line.  The reference arm (`--impl reference`) times
+the CPU oracle (oracle/, plain C) on this box's host cores on a bounded sample
+of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "1080p unified mesh+3DGS render frames/s (device-timed)"
+UNIT = "frames/s"
+WORKLOAD = ("multiview: mip360-like 3M Gaussians (SH3) + 200k-triangle textured sphere+torus, "
+            "256-view 1920x1080 orbit, views sharded i mod N")
+
+# ALU roofline of the blend: algorithmic lane-ops per unit of work
+OPS_GAUSS_TEST = 11      # dx, dy, 4 mul, 2 fma, compare
+OPS_GAUSS_FRAG = 12      # -q/2, exp, *o, min, T*a, 3 fma colour, T update (+ entity close test)
+OPS_TRI_TEST = 33        # 3 int64 edge functions at the centre + 12 sample offsets + 12 compares
+OPS_TRI_FRAG = 60        # fp64 perspective barycentrics, bilinear texture, entity update
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--views", type=int, default=16, help="views per rank per step")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n-gauss", type=int, default=3_000_000)
+    ap.add_argument("--sort-mode", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gather", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------
+# clocks sampling during the timed region
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            if self.t:
+                self.t.join(timeout=2)
+
+    def summary(self):
+        rows = [r for r in self.rows if len(r) >= 7 and r[0].isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [int(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------
+# reference arm: the CPU oracle on the host cores
+# ----------------------------------------------------------------------------
+def oracle_frames(scene, cams, threads: int):
+    """project + bin + full-frame render through the oracle; returns seconds per frame."""
+    import oracle
+    o = oracle.Oracle(scene.gaussians, scene.mesh, threads=threads)
+    st = oracle.scene_settings(scene)
+    times = []
+    for cam in cams:
+        t0 = time.perf_counter()
+        o.full(cam, **st)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    from paper_2601_19233_b200 import scenes
+    sc = scenes.make_multiview(n=a.n_gauss)
+    cores = host_cores()
+    # bounded sample: each step is one full 1080p view of the orbit through the oracle
+    # (~2-5 s per view); warm-up and timed steps are capped so the run ends in minutes.
+    warm = min(a.warmup, 1)
+    steps = max(1, min(a.steps, 6))
+    cams = [sc.cameras[(i * 37) % len(sc.cameras)] for i in range(warm + steps)]
+    oracle_frames(sc, cams[:warm], cores)
+    times = oracle_frames(sc, cams[warm:], cores)
+    total = sum(times)
+    fps = steps / total
+    sample = f"{steps} full 1080p views of the 256-view orbit (project + bin + render), {warm} warm-up view"
+    line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": steps, "warmup": warm, "ms_per_step": 1000 * total / steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "views_per_step_per_gpu": 1, "engine": "CPU oracle (plain C, OpenMP)"},
+            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def alg_bytes(N, F, V, N_vis, F_vis, P, K, W, H, sh_k=16):
+    """Algorithmic HBM bytes of one frame: inputs once (SH of visible
+    Gaussians only), records written once, pairs written once + sorted once + read for
+    ranges + read with records in the blend, output once."""
+    return (N * 44 + N_vis * sh_k * 12 + V * 20 + F * 16 + N_vis * 48 + F_vis * 96 + P * 12
+            + K * (12 + 24 + 8 + 4 + 48) + W * H * 16)
+
+
+def run_ours(a, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2601_19233_b200 import renderer as R, scenes
+    from paper_2601_19233_b200.dist import gather_frames, views_for_rank
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    sc = scenes.make_multiview(n=a.n_gauss)
+    n_orbit = len(sc.cameras)
+    W, H = sc.cameras[0].width, sc.cameras[0].height
+    r = R.Renderer(sc.gaussians.count, sc.mesh.num_triangles, 20 << 20, W, H, bg=tuple(float(v) for v in sc.bg),
+                   sort_mode=a.sort_mode)
+    ds = R.to_device(sc, dev)
+    V = a.views
+
+    def views_of(step):
+        return views_for_rank(step, V, rank, world, n_orbit)
+
+    frames = [torch.empty((V, H, W, 4), dtype=torch.float32, device=dev) for _ in range(2)]
+    gather = world > 1 and not a.no_gather
+    recv = None
+    if gather and rank == 0:
+        recv = [torch.empty((world - 1, V, H, W, 4), dtype=torch.float32, device=dev) for _ in range(2)]
+    comm = torch.cuda.Stream(device=dev) if gather else None
+    s = torch.cuda.current_stream()
+
+    def step_fn(step, ev_pairs=None):
+        buf = frames[step & 1]
+        for j, vi in enumerate(views_of(step)):
+            r.preprocess(ds, sc.cameras[vi])
+            r.bin()
+            if ev_pairs is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                r.render(buf[j])
+                e1.record(s)
+                ev_pairs.append((e0, e1))
+            else:
+                r.render(buf[j])
+        if not gather:
+            return []
+        done = torch.cuda.Event()
+        done.record(s)
+        with torch.cuda.stream(comm):
+            comm.wait_event(done)
+            return gather_frames(buf, recv[step & 1] if rank == 0 else None, rank, world)
+
+    # warm-up (also validates capacity)
+    pending = []
+    for w in range(a.warmup):
+        for q in pending:
+            q.wait()
+        pending = step_fn(w)
+    for q in pending:
+        q.wait()
+    torch.cuda.synchronize()
+    st = r.stats()
+    assert st["overflow"] == 0
+
+    # work counts + frame-level bytes for the views of the timed region (untimed pass)
+    work = dict(gauss_tests=0, gauss_frags=0, tri_tests=0, tri_frags=0)
+    bytes_alg = 0.0
+    K_sum = 0
+    tmp = torch.empty((H, W, 4), dtype=torch.float32, device=dev)
+    timed_views = [vi for k in range(a.steps) for vi in views_of(a.warmup + k)]
+    for vi in timed_views:
+        cam = sc.cameras[vi]
+        r.preprocess(ds, cam)
+        r.bin()
+        _, wk = r.render_counted(tmp)
+        for k2 in work:
+            work[k2] += wk[k2]
+        stt = r.stats()
+        K_sum += stt["num_pairs"]
+        bytes_alg += alg_bytes(sc.gaussians.count, sc.mesh.num_triangles, sc.mesh.num_vertices,
+                               stt["visible_gaussians"], stt["visible_triangles"],
+                               sc.gaussians.count + sc.mesh.num_triangles, stt["num_pairs"], W, H)
+    torch.cuda.synchronize()
+
+    # ---- timed region ---------------------------------------------------------
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.2)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = r.launch_count()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    blend_ev = []
+    t_start.record(s)
+    pending = []
+    for k in range(a.steps):
+        new = step_fn(a.warmup + k, blend_ev)
+        for q in pending:  # frames of step k-1 must have left before buffer k+1 is rewritten
+            q.wait()
+        pending = new
+    for q in pending:
+        q.wait()
+    t_end.record(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks.stop()
+    launches = r.launch_count() - launches0
+    ms = t_start.elapsed_time(t_end)
+    blend_ms = sum(e0.elapsed_time(e1) for e0, e1 in blend_ev) / max(len(blend_ev), 1)
+    t = torch.tensor([ms, blend_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, blend_max = float(t[0]), float(t[1])
+    frames_total = world * V * a.steps
+    value = frames_total / (ms_max / 1000.0)
+
+    # ---- end-to-end through the host-buffer C-ABI call -------------------------
+    e2e = None
+    if not a.no_e2e:
+        host = R.to_pinned(sc)
+        h2d = host.nbytes()
+        out_h = torch.empty((V, H, W, 4), dtype=torch.float32).pin_memory()
+        cams0 = [sc.cameras[vi] for vi in views_of(0)]
+        r.render_host(host, cams0, out_h)  # warm-up (allocates staging)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for k in range(a.e2e_steps):
+            r.render_host(host, [sc.cameras[vi] for vi in views_of(k)], out_h)
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * V * a.e2e_steps / float(dt[0]), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": V * H * W * 16, "steps": a.e2e_steps,
+               "path": "unimgs_render_host: pinned host scene -> device, per-view pipeline, frames -> pinned host"}
+
+    # ---- CPU baseline (oracle), rank 0 at N = 1 only ---------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cores = host_cores()
+        cams = [sc.cameras[0], sc.cameras[128]]
+        oracle_frames(sc, cams[:1], cores)  # warm (page-in)
+        times = oracle_frames(sc, cams, cores)
+        cpu = {"value": len(times) / sum(times), "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": "views 0 and 128 of the orbit, full 1080p frame each (project + bin + render), "
+                         "after one warm-up view"}
+
+    if rank != 0:
+        return
+    # ---- roofline of the dominant kernel (blend, ALU/issue-bound) -----------------
+    n_blend = len(timed_views)
+    ops = (work["gauss_tests"] * OPS_GAUSS_TEST + work["gauss_frags"] * OPS_GAUSS_FRAG
+           + work["tri_tests"] * OPS_TRI_TEST + work["tri_frags"] * OPS_TRI_FRAG) / n_blend
+    import torch as _t
+    props = _t.cuda.get_device_properties(dev)
+    sm_count = props.multi_processor_count
+    peak_tops = sm_count * 128 * 1.965e9 / 1e12  # 4 schedulers x 32 lanes x max clock
+    achieved = ops / (blend_max / 1000.0) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "blend_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    peaks = {}
+    pp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pp):
+        peaks = json.load(open(pp))
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    frame_ms = ms_max / (V * a.steps)
+    hbm_gbs = bytes_alg / len(timed_views) / (frame_ms / 1000.0) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "views_per_step_per_gpu": V, "image": [W, H],
+                   "gaussians": sc.gaussians.count, "triangles": sc.mesh.num_triangles,
+                   "sort_mode": a.sort_mode, "gather": "NCCL send/recv to rank 0" if gather else "none",
+                   "l2": "inputs larger than L2 (scene %.2f GB > 126 MB; per-view K ~7.5M pairs)" % (ds.nbytes() / 1e9),
+                   "parallelism": f"views i mod {world}"},
+        "frame_ms": frame_ms,
+        "roofline": {"bound": "alu", "kernel": "k_blend", "achieved": achieved, "peak": peak_tops,
+                     "unit": "Tops/s", "frac": achieved / peak_tops, "traffic": traffic,
+                     "ops_per_launch": ops, "avg_launch_ms": blend_max,
+                     "peak_note": f"{sm_count} SMs x 4 schedulers x 32 lanes x 1965 MHz (issue-slot lane-ops)",
+                     "work_per_launch": {k: v / n_blend for k, v in work.items()}},
+        "hbm": {"alg_bytes_per_frame": bytes_alg / len(timed_views), "achieved_gbs": hbm_gbs,
+                "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak,
+                "peak_note": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+        "blend_share": blend_max / frame_ms,
+        "clocks": clocks.summary(),
+        "gpu_launches": launches,
+        "launches_per_frame": launches / (V * a.steps),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "stats_last_view": {k: st[k] for k in ("num_pairs", "visible_gaussians", "visible_triangles",
+                                                "max_tile_pairs")},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(a, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -168,6 +168,12 @@ UNIMGS_API int unimgs_bin(unimgs_ctx *c, void *stream);
  * Must follow unimgs_bin. */
 UNIMGS_API int unimgs_render(unimgs_ctx *c, float *out_rgbt, void *stream);
 
+/* Measurement variant of unimgs_render: identical output, plus the blend's
+ * work counts (host work[4]): Gaussian entries tested, Gaussian fragments
+ * blended, triangle entries tested, triangle fragments blended, summed over
+ * pixels up to each pixel's termination.  Synchronises `stream`. */
+UNIMGS_API int unimgs_render_counted(unimgs_ctx *c, float *out_rgbt, int64_t *work, void *stream);
+
 /* Synchronise `stream` and report the last frame's counters (host *out). */
 UNIMGS_API int unimgs_get_stats(unimgs_ctx *c, unimgs_stats *out, void *stream);
 

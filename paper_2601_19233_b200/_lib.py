@@ -9,14 +9,14 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libunimgs.so")
+LIB_PATH = os.environ.get("UNIMGS_LIB", os.path.join(HERE, "libunimgs.so"))  # override: experiments only
 
 OK, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED, ERR_CAPACITY, ERR_CUDA, ERR_STATE = range(6)
 STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "UNSUPPORTED", 3: "CAPACITY", 4: "CUDA", 5: "STATE"}
 
 # every symbol include/unimgs.h declares
 EXPORTS = ("unimgs_default_settings", "unimgs_create", "unimgs_set_settings", "unimgs_reserve", "unimgs_reserve2",
-           "unimgs_preprocess", "unimgs_bin", "unimgs_render", "unimgs_get_stats", "unimgs_get_bins",
+           "unimgs_preprocess", "unimgs_bin", "unimgs_render", "unimgs_render_counted", "unimgs_get_stats", "unimgs_get_bins",
            "unimgs_get_records", "unimgs_render_host", "unimgs_launch_count", "unimgs_error_string",
            "unimgs_destroy")
 
@@ -73,6 +73,7 @@ def load():
     L.unimgs_preprocess.argtypes = [vp, C.POINTER(Gaussians), C.POINTER(Mesh), C.POINTER(Camera), vp]
     L.unimgs_bin.argtypes = [vp, vp]
     L.unimgs_render.argtypes = [vp, vp, vp]
+    L.unimgs_render_counted.argtypes = [vp, vp, vp, vp]
     L.unimgs_get_stats.argtypes = [vp, C.POINTER(Stats), vp]
     L.unimgs_get_bins.argtypes = [vp, vp, vp, vp, vp]
     L.unimgs_get_records.argtypes = [vp, vp, vp, vp, vp, vp, vp]
@@ -84,7 +85,7 @@ def load():
     L.unimgs_destroy.argtypes = [vp]
     L.unimgs_destroy.restype = None
     for name in ("unimgs_create", "unimgs_set_settings", "unimgs_reserve", "unimgs_reserve2", "unimgs_preprocess",
-                 "unimgs_bin", "unimgs_render", "unimgs_get_stats", "unimgs_get_bins", "unimgs_get_records",
+                 "unimgs_bin", "unimgs_render", "unimgs_render_counted", "unimgs_get_stats", "unimgs_get_bins", "unimgs_get_records",
                  "unimgs_render_host"):
         getattr(L, name).restype = C.c_int
     _lib = L

@@ -274,6 +274,23 @@ extern "C" int unimgs_render(unimgs_ctx *c, float *out, void *stream) {
     return check_launch(c, "render");
 }
 
+extern "C" int unimgs_render_counted(unimgs_ctx *c, float *out, int64_t *work_host, void *stream) {
+    if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (c->stage < 2) return fail(c, UNIMGS_ERR_STATE, "render before bin");
+    if (!out || !work_host) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "out/work is NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    CUDA_TRY(c, cudaMemsetAsync(c->buf.st->work, 0, sizeof(c->buf.st->work), s));
+    BlendParams bp{c->set.alpha_max, c->set.t_eps, c->set.bg_alpha, {c->set.bg[0], c->set.bg[1], c->set.bg[2]}};
+    c->launches += launch_blend(c->buf, c->g, c->m, c->cam, bp, out, s, true);
+    int rc = check_launch(c, "render_counted");
+    if (rc) return rc;
+    unsigned long long w[4];
+    CUDA_TRY(c, cudaMemcpyAsync(w, c->buf.st->work, sizeof w, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    for (int k = 0; k < 4; k++) work_host[k] = (int64_t)w[k];
+    return UNIMGS_OK;
+}
+
 extern "C" int unimgs_get_stats(unimgs_ctx *c, unimgs_stats *out, void *stream) {
     if (!c || !out) return UNIMGS_ERR_INVALID_ARGUMENT;
     if (!c->reserved) return fail(c, UNIMGS_ERR_STATE, "stats before reserve");

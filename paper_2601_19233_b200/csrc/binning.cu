@@ -5,35 +5,50 @@
 // (tile, bits(depth), unified id) -- the lexicographic order of the 64-bit key
 // tile << 32 | bits(depth) with ties by id (readings R8, R9, R23).
 //
-// Two schedules produce the identical order:
+// Pipeline (both sort modes produce the identical order):
+//   k_compact        visible primitives in id order (decoupled look-back scan)
+//                    and every digit histogram the radix passes need: depth
+//                    digits per primitive, tile digits of all pairs computed
+//                    per rect row (no per-pair atomics);
+//   k_tile_lo_hist   low tile digit histogram from its difference array.
 //   sort_mode 0 (factored, default):
-//     compact visible primitives (id order) -> 4 stable 8-bit onesweep passes
-//     on the 32-bit depth key -> scan of tiles_touched in depth order fused
-//     with the pair duplication (u16 tile id + u32 primitive id) -> stable
-//     onesweep passes on the tile id only (2 for <= 2^16 tiles) -> ranges.
-//     Stable LSD by tile over pairs emitted in (depth, id) order IS the
-//     (tile, depth, id) order; it moves ~4x fewer bytes than sorting K
-//     64-bit keys over 32 + tile_bits bits.
-//   sort_mode 1 (full): scan of tiles_touched in id order fused with the
-//     duplication of 64-bit keys -> onesweep over bits [0, 32 + tile_bits).
+//     k_onesweep<u32> x4   stable LSD on the 32-bit depth key of the visible
+//                          primitives (id ties stay in id order);
+//     k_duplicate<false>   scan of tiles_touched in depth order fused with the
+//                          emission of (u16 tile, u32 id) pairs, staged through
+//                          shared memory so every store is coalesced;
+//     k_onesweep<u16> x2   stable LSD on the tile id: pairs emitted in
+//                          (depth, id) order come out in (tile, depth, id)
+//                          order -- ~4x fewer bytes than sorting K 64-bit keys;
+//     k_ranges16           tile ranges from the sorted tile ids.
+//   sort_mode 1 (full, the literal form):
+//     k_duplicate<true>    (tile << 32 | depth, id) pairs in id order;
+//     k_onesweep<u64> x(4 + ceil(tile_bits/8)) over bits [0, 32 + tile_bits);
+//     k_ranges64.
 //
-// All scans are single-pass decoupled look-back (tile index claimed from an
-// atomic counter for forward progress).  Look-back entries are 64-bit
-// {epoch tag << 2 | flag, value}: the tag changes every pass of every frame,
-// so the buffers are never cleared and the pipeline stays graph-capturable.
+// Scans and sort passes are single-pass decoupled look-back over tiles claimed
+// from an atomic counter (forward progress).  Look-back entries are 64-bit
+// {epoch tag << 2 | flag, value}; the tag changes every pass of every frame, so
+// nothing is cleared between frames and the whole frame is graph-capturable.
 #include <algorithm>
+#include <type_traits>
 
 #include "internal.cuh"
+
+#ifndef UNIMGS_SORT_ITEMS
+#define UNIMGS_SORT_ITEMS 16
+#endif
 
 namespace unimgs {
 
 constexpr unsigned kFlagAgg = 1, kFlagInc = 2;
 constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
-constexpr int kSortThreads = 256, kSortItems = 16, kSortTile = kSortThreads * kSortItems;
+constexpr int kSortThreads = 256, kSortItems = UNIMGS_SORT_ITEMS, kSortTile = kSortThreads * kSortItems;
+constexpr int kLookWin = 4;  // predecessors inspected per look-back round trip
 
 // scan/pass slots (select the dynamic tile counter and the epoch tag)
-enum { SLOT_COMPACT = 0, SLOT_DEPTH0 = 1, SLOT_DUP = 5, SLOT_TILE0 = 6, SLOT_FULLDUP = 0, SLOT_FULL0 = 1 };
-// histogram rows: factored: 0..3 depth digits, 4..5 tile digits; full: 0..3 depth, 4..5 tile
+enum { SLOT_COMPACT = 0, SLOT_DUP = 1, SLOT_PASS0 = 2 };
+// histogram rows: 0..3 depth digits, 4..5 tile digits (weighted by pairs in mode 1)
 enum { HIST_DEPTH0 = 0, HIST_TILE0 = 4 };
 
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
@@ -141,108 +156,226 @@ __device__ __forceinline__ void scan_lookback(const unsigned (&val)[ITEMS], unsi
     total = s_w[8];
 }
 
-__device__ __forceinline__ void flush_hist(unsigned *s_h, unsigned *g_h, int n) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const unsigned v = s_h[i];
-        if (v) atomicAdd(g_h + i, v);
+// Same scan for a warp-striped arrangement: item i of lane l of warp w is element
+// base + w * 32 * ITEMS + i * 32 + l (coalesced loads); offsets follow index order.
+template <int ITEMS>
+__device__ __forceinline__ void scan_lookback_striped(const unsigned (&val)[ITEMS], unsigned (&excl)[ITEMS],
+                                                      unsigned tile, unsigned long long *lb, unsigned tag,
+                                                      unsigned *s_w, unsigned &total) {
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned carry = 0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        unsigned x = val[i];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (unsigned)o) x = sat_add(x, y);
+        }
+        const unsigned e = __shfl_up_sync(0xffffffffu, x, 1);
+        excl[i] = sat_add(carry, lane ? e : 0u);
+        carry = sat_add(carry, __shfl_sync(0xffffffffu, x, 31));
+    }
+    // reuse the blocked scan for the warp totals: lane 0 contributes its warp's total
+    unsigned wv[1] = {lane == 0 ? carry : 0u}, wx[1];
+    scan_lookback<1>(wv, wx, tile, lb, tag, s_w, total);
+    const unsigned wbase = __shfl_sync(0xffffffffu, wx[0], 0);
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) excl[i] = sat_add(wbase, excl[i]);
+}
+
+// Tile-digit histograms of a primitive's pairs, per rect row: the low digit
+// (t & 255) of a run of consecutive tile ids is a cyclic range of bins
+// (difference array d_lo[257] + full cycles), the high digit (t >> 8) takes
+// one or two values.  Exact pair counts with O(rows) shared atomics.
+__device__ __forceinline__ void tile_digit_hist(uint2 r, int tiles_x, unsigned *d_lo, unsigned *h_hi,
+                                                unsigned *all_lo) {
+    const unsigned x0 = r.x & 0xFFFF, y0 = r.x >> 16, x1 = r.y & 0xFFFF, y1 = r.y >> 16;
+    for (unsigned ty = y0; ty <= y1; ty++) {
+        const unsigned a = ty * (unsigned)tiles_x + x0, b = ty * (unsigned)tiles_x + x1;
+        const unsigned len = b - a + 1, full = len >> 8, rem = len & 255u;
+        if (full) atomicAdd(all_lo, full);
+        if (rem) {
+            const unsigned lo = a & 255u, e = lo + rem;
+            if (e <= 256u) {
+                atomicAdd(d_lo + lo, 1u);
+                atomicAdd(d_lo + e, 0xFFFFFFFFu);
+            } else {
+                atomicAdd(d_lo + lo, 1u);
+                atomicAdd(d_lo + 256, 0xFFFFFFFFu);
+                atomicAdd(d_lo + 0, 1u);
+                atomicAdd(d_lo + (e - 256u), 0xFFFFFFFFu);
+            }
+        }
+        for (unsigned h = a >> 8; h <= (b >> 8); h++) {
+            const unsigned s0 = max(a, h << 8), s1 = min(b, (h << 8) + 255u);
+            atomicAdd(h_hi + (h & 255u), s1 - s0 + 1);
+        }
     }
 }
 
 // ----------------------------------------------------------------------------
-// sort_mode 0, step 1: compact visible primitives in id order; depth-digit
-// histograms for the 4 depth passes.
+// k_compact: visible primitives (touched > 0) in id order -> (depth key, id),
+// warp-striped (coalesced) with a ballot scan.  Histograms for the radix
+// passes: depth digits of the primitive keys (factored) or of the pair keys
+// (FULL: weighted by tiles_touched), and the two tile digits of all pairs.
 // ----------------------------------------------------------------------------
+template <bool FULL>
 __global__ void __launch_bounds__(kScanThreads) k_compact(int64_t P, const uint32_t *__restrict__ touched,
-                                                          const uint32_t *__restrict__ dkey, uint32_t *ok,
-                                                          uint32_t *ov, unsigned long long *lb, DevState *st) {
+                                                          const uint32_t *__restrict__ dkey,
+                                                          const uint2 *__restrict__ rect, int tiles_x, int tile_bits,
+                                                          uint32_t *ok, uint32_t *ov, unsigned long long *lb,
+                                                          DevState *st) {
     __shared__ unsigned s_w[10], s_tile;
     __shared__ unsigned s_h[4 * 256];
+    __shared__ unsigned s_dlo[257], s_hhi[256], s_all;
     const unsigned tag = epoch_tag(st, SLOT_COMPACT);
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     while (true) {
         const unsigned tile = claim_tile(&st->ctr[SLOT_COMPACT], &s_tile);
         const int64_t base = (int64_t)tile * kScanTile;
         if (base >= P) break;
         for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) s_h[i] = 0;
-        unsigned v[kScanItems], ex[kScanItems];
-        const int64_t b0 = base + (int64_t)threadIdx.x * kScanItems;  // blocked arrangement
+        for (int i = threadIdx.x; i < 257; i += blockDim.x) s_dlo[i] = 0;
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_hhi[i] = 0;
+        if (threadIdx.x == 0) s_all = 0;
+        unsigned v[kScanItems], ex[kScanItems], tt[kScanItems];
+        const int64_t b0 = base + (int64_t)wid * 32 * kScanItems + lane;  // warp-striped
 #pragma unroll
-        for (int i = 0; i < kScanItems; i++) v[i] = (b0 + i < P && touched[b0 + i] > 0) ? 1u : 0u;
+        for (int i = 0; i < kScanItems; i++) {
+            tt[i] = b0 + 32 * i < P ? touched[b0 + 32 * i] : 0u;
+            v[i] = tt[i] > 0 ? 1u : 0u;
+        }
         unsigned total;
-        scan_lookback<kScanItems>(v, ex, tile, lb, tag, s_w, total);
+        scan_lookback_striped<kScanItems>(v, ex, tile, lb, tag, s_w, total);
 #pragma unroll
         for (int i = 0; i < kScanItems; i++) {
             if (v[i]) {
-                const uint32_t k = dkey[b0 + i];
+                const int64_t p = b0 + 32 * i;
+                const uint32_t k = dkey[p];
                 ok[ex[i]] = k;
-                ov[ex[i]] = (uint32_t)(b0 + i);
+                ov[ex[i]] = (uint32_t)p;
+                const unsigned w = FULL ? tt[i] : 1u;
 #pragma unroll
-                for (int d = 0; d < 4; d++) atomicAdd(&s_h[d * 256 + ((k >> (8 * d)) & 255u)], 1u);
+                for (int d = 0; d < 4; d++) atomicAdd(&s_h[d * 256 + ((k >> (8 * d)) & 255u)], w);
+                tile_digit_hist(rect[p], tiles_x, s_dlo, s_hhi, &s_all);
             }
         }
         __syncthreads();
-        flush_hist(s_h, &st->hist[HIST_DEPTH0][0], 4 * 256);
+        for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
+            const unsigned h = s_h[i];
+            if (h) atomicAdd(&st->hist[HIST_DEPTH0][0] + i, h);
+        }
+        for (int i = threadIdx.x; i < 257; i += blockDim.x) {
+            const unsigned h = s_dlo[i];
+            if (h) atomicAdd(&st->tdlo[i], h);
+        }
+        if (tile_bits > 8)
+            for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+                const unsigned h = s_hhi[i];
+                if (h) atomicAdd(&st->hist[HIST_TILE0 + 1][i], h);
+            }
+        if (threadIdx.x == 0 && s_all) atomicAdd(&st->tdlo_all, s_all);
         if (base + kScanTile >= P && threadIdx.x == 0) st->n_vis = total;
     }
 }
 
+// Tile low-digit histogram from its difference array (one CTA of 256 threads).
+__global__ void k_tile_lo_hist(DevState *st) {
+    __shared__ unsigned s_ws[8];
+    const unsigned t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    unsigned x = st->tdlo[t];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (unsigned)o) x += y;
+    }
+    if (lane == 31) s_ws[wid] = x;
+    __syncthreads();
+    unsigned add = 0;
+    for (unsigned w = 0; w < wid; w++) add += s_ws[w];
+    st->hist[HIST_TILE0][t] = x + add + st->tdlo_all;
+}
+
 // ----------------------------------------------------------------------------
-// Duplication fused into the tiles_touched scan.  FULL = false: items are the
-// depth-sorted visible primitives, pairs are (u16 tile, id).  FULL = true:
-// items are all primitives in id order, pairs are (tile << 32 | depth, id).
+// k_duplicate: tiles_touched scan over the (depth-sorted or id-ordered) visible
+// primitives fused with the pair emission.  Each CTA's pairs form one
+// contiguous range; they are written into shared memory in windows of CAP pairs
+// by the owning threads, then copied out with coalesced stores.
 // ----------------------------------------------------------------------------
 template <bool FULL>
-__global__ void __launch_bounds__(kScanThreads) k_duplicate(int64_t P_all, const uint32_t *__restrict__ ids,
+struct DupCfg {
+    static constexpr int CAP = FULL ? 4096 : 8192;
+    using Key = typename std::conditional<FULL, unsigned long long, uint16_t>::type;
+};
+
+template <bool FULL>
+__global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t *__restrict__ ids,
                                                             const uint32_t *__restrict__ touched,
                                                             const uint2 *__restrict__ rect,
                                                             const uint32_t *__restrict__ dkey, int tiles_x,
-                                                            int tile_bits, int64_t cap, void *tk_, uint32_t *tv,
+                                                            int64_t cap, void *tk_, uint32_t *tv,
                                                             unsigned long long *lb, DevState *st) {
-    __shared__ unsigned s_w[10], s_tile;
-    __shared__ unsigned s_h[6 * 256];
-    const int slot = FULL ? SLOT_FULLDUP : SLOT_DUP;
-    const unsigned tag = epoch_tag(st, slot);
-    const int64_t n = FULL ? P_all : (int64_t)st->n_vis;
-    const int nh = FULL ? 6 : 2;
+    using Key = typename DupCfg<FULL>::Key;
+    constexpr int CAP = DupCfg<FULL>::CAP;
+    extern __shared__ __align__(16) unsigned char smem[];
+    Key *s_k = reinterpret_cast<Key *>(smem);
+    uint32_t *s_v = reinterpret_cast<uint32_t *>(s_k + CAP);
+    __shared__ unsigned s_w[10], s_tile, s_base;
+    Key *tk = reinterpret_cast<Key *>(tk_);
+    const unsigned tag = epoch_tag(st, SLOT_DUP);
+    const int64_t n = (int64_t)st->n_vis;
+    const unsigned capu = (unsigned)(cap < 0xFFFFFFFFll ? cap : 0xFFFFFFFFll);
     while (true) {
-        const unsigned tile = claim_tile(&st->ctr[slot], &s_tile);
+        const unsigned tile = claim_tile(&st->ctr[SLOT_DUP], &s_tile);
         const int64_t base = (int64_t)tile * kScanTile;
         if (base >= n) break;
-        for (int i = threadIdx.x; i < nh * 256; i += blockDim.x) s_h[i] = 0;
         unsigned v[kScanItems], ex[kScanItems];
         uint32_t id[kScanItems];
-        const int64_t b0 = base + (int64_t)threadIdx.x * kScanItems;
+        const int64_t b0 = base + (int64_t)(threadIdx.x >> 5) * 32 * kScanItems + (threadIdx.x & 31);  // warp-striped
 #pragma unroll
         for (int i = 0; i < kScanItems; i++) {
-            const bool in = b0 + i < n;
-            id[i] = in ? (FULL ? (uint32_t)(b0 + i) : ids[b0 + i]) : 0u;
+            const bool in = b0 + 32 * i < n;
+            id[i] = in ? ids[b0 + 32 * i] : 0u;
             v[i] = in ? touched[id[i]] : 0u;
         }
         unsigned total;
-        scan_lookback<kScanItems>(v, ex, tile, lb, epoch_tag(st, slot), s_w, total);
-        for (int i = 0; i < kScanItems; i++) {
-            if (!v[i]) continue;
-            const uint2 r = rect[id[i]];
-            const int x0 = r.x & 0xFFFF, y0 = r.x >> 16, x1 = r.y & 0xFFFF, y1 = r.y >> 16;
-            const uint32_t dk = FULL ? dkey[id[i]] : 0u;
-            int64_t pos = ex[i];
-            for (int ty = y0; ty <= y1; ty++)
-                for (int tx = x0; tx <= x1; tx++, pos++) {
-                    const unsigned t = (unsigned)(ty * tiles_x + tx);
-                    if (pos < cap) {
-                        if (FULL) reinterpret_cast<unsigned long long *>(tk_)[pos] = ((unsigned long long)t << 32) | dk;
-                        else reinterpret_cast<uint16_t *>(tk_)[pos] = (uint16_t)t;
-                        tv[pos] = id[i];
-                    }
-                    if (FULL) {
+        scan_lookback_striped<kScanItems>(v, ex, tile, lb, tag, s_w, total);
+        if (threadIdx.x == 0) s_base = ex[0];
+        uint2 r[kScanItems];
+        uint32_t dk[kScanItems];
 #pragma unroll
-                        for (int d = 0; d < 4; d++) atomicAdd(&s_h[d * 256 + ((dk >> (8 * d)) & 255u)], 1u);
-                    }
-                    atomicAdd(&s_h[(FULL ? 4 : 0) * 256 + (t & 255u)], 1u);
-                    if (tile_bits > 8) atomicAdd(&s_h[(FULL ? 5 : 1) * 256 + ((t >> 8) & 255u)], 1u);
-                }
+        for (int i = 0; i < kScanItems; i++) {
+            r[i] = v[i] ? rect[id[i]] : make_uint2(0u, 0u);
+            dk[i] = (FULL && v[i]) ? dkey[id[i]] : 0u;
         }
         __syncthreads();
-        flush_hist(s_h, &st->hist[FULL ? 0 : HIST_TILE0][0], nh * 256);
+        const unsigned pbase = s_base, pend = min(total, capu);
+        for (unsigned wb = pbase; wb < pend; wb += CAP) {
+            const unsigned we = min(pend, wb + CAP);
+#pragma unroll
+            for (int i = 0; i < kScanItems; i++) {
+                if (!v[i]) continue;
+                const unsigned lo = max(ex[i], wb), hi = min(ex[i] + v[i], we);
+                if (lo >= hi) continue;
+                const unsigned x0 = r[i].x & 0xFFFF, y0 = r[i].x >> 16, x1 = r[i].y & 0xFFFF;
+                const unsigned wdt = x1 - x0 + 1, l0 = lo - ex[i];
+                unsigned tx = x0 + l0 % wdt, ty = y0 + l0 / wdt;
+                for (unsigned g = lo; g < hi; g++) {
+                    const unsigned t = ty * (unsigned)tiles_x + tx;
+                    if (FULL) s_k[g - wb] = (Key)(((unsigned long long)t << 32) | dk[i]);
+                    else s_k[g - wb] = (Key)t;
+                    s_v[g - wb] = id[i];
+                    if (++tx > x1) { tx = x0; ty++; }
+                }
+            }
+            __syncthreads();
+            for (unsigned k = threadIdx.x; k < we - wb; k += kScanThreads) {
+                tk[wb + k] = s_k[k];
+                tv[wb + k] = s_v[k];
+            }
+            __syncthreads();
+        }
         if (base + kScanTile >= n && threadIdx.x == 0) {
             st->needed = total;
             const bool over = (int64_t)total > cap;
@@ -250,31 +383,31 @@ __global__ void __launch_bounds__(kScanThreads) k_duplicate(int64_t P_all, const
             st->K = over ? 0u : total;
         }
     }
-    (void)tag;
 }
 
 // ----------------------------------------------------------------------------
 // One stable onesweep LSD pass on `bits` bits at `shift` (Adinets & Merrill).
-// Tiles of 4096 keys, warp-striped; warp-level multisplit ranking with
-// __match_any_sync; per-digit decoupled look-back; scatter through smem.
+// Tiles of 256 x ITEMS keys, warp-striped; warp-level multisplit ranking with
+// __match_any_sync; keys are moved into shared memory at their block-sorted
+// position BEFORE the per-digit decoupled look-back (so no key register is live
+// across it); then a coalesced-by-digit scatter to global memory.
 // ----------------------------------------------------------------------------
 template <typename KT>
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(const KT *__restrict__ kin, const uint32_t *__restrict__ vin,
-                                                           KT *__restrict__ kout, uint32_t *__restrict__ vout,
-                                                           const unsigned *n_ptr, int shift, int bits,
-                                                           const unsigned *hist, int slot,
-                                                           unsigned long long *lb, DevState *st) {
+__global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(const KT *__restrict__ kin,
+                                                              const uint32_t *__restrict__ vin, KT *__restrict__ kout,
+                                                              uint32_t *__restrict__ vout, const unsigned *n_ptr,
+                                                              int shift, int bits, const unsigned *hist, int slot,
+                                                              unsigned long long *lb, DevState *st) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned *s_wh = reinterpret_cast<unsigned *>(smem);           // [8][256]
     unsigned *s_doff = s_wh + 8 * 256;                              // [256] block-local digit offsets
     int *s_glob = reinterpret_cast<int *>(s_doff + 256);            // [256] global base - local offset
     unsigned *s_hex = reinterpret_cast<unsigned *>(s_glob + 256);   // [256] global exclusive histogram
-    unsigned *s_misc = s_hex + 256;                                 // [4]
-    KT *s_k = reinterpret_cast<KT *>(s_misc + 4);
+    unsigned *s_misc = s_hex + 256;                                 // [16]
+    KT *s_k = reinterpret_cast<KT *>(s_misc + 16);
     uint32_t *s_v = reinterpret_cast<uint32_t *>(s_k + kSortTile);
 
     const unsigned n = *n_ptr;
-    if (st->overflow && n_ptr == &st->K) return;
     const unsigned tag = epoch_tag(st, slot);
     const unsigned mask = (1u << bits) - 1u;
     const unsigned t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -288,26 +421,23 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const KT *__restrict_
             const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= (unsigned)o) x += y;
         }
-        if (lane == 31) s_misc[0] = 0;  // placeholder to keep s_misc initialised
-        __shared__ unsigned s_ws[8];
-        if (lane == 31) s_ws[wid] = x;
+        if (lane == 31) s_misc[8 + wid] = x;
         __syncthreads();
         unsigned add = 0;
-        for (unsigned w = 0; w < wid; w++) add += s_ws[w];
+        for (unsigned w = 0; w < wid; w++) add += s_misc[8 + w];
         s_hex[t] = x - h + add;
     }
 
     while (true) {
         const unsigned tile = claim_tile(&st->ctr[slot], &s_misc[1]);
-        const unsigned base = tile * (unsigned)kSortTile;
         if ((unsigned long long)tile * kSortTile >= n) break;
+        const unsigned base = tile * (unsigned)kSortTile;
         for (int i = t; i < 8 * 256; i += kSortThreads) s_wh[i] = 0;
         __syncthreads();
 
         KT key[kSortItems];
         uint32_t val[kSortItems];
         unsigned rank[kSortItems];
-        unsigned dig[kSortItems];
         const unsigned wbase = base + wid * 32u * kSortItems + lane;
         const unsigned lt = lanemask_lt();
         unsigned *wh = s_wh + wid * 256;
@@ -317,11 +447,11 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const KT *__restrict_
             const bool valid = idx < n;
             key[i] = valid ? kin[idx] : (KT)0;
             val[i] = valid ? vin[idx] : 0u;
-            dig[i] = valid ? (unsigned)((key[i] >> shift) & mask) : 256u;
         }
 #pragma unroll
         for (int i = 0; i < kSortItems; i++) {
-            const unsigned d = dig[i];
+            const bool valid = wbase + 32u * i < n;
+            const unsigned d = valid ? (unsigned)((key[i] >> shift) & mask) : 256u;
             const unsigned peers = __match_any_sync(0xffffffffu, d);
             const unsigned before = d < 256u ? wh[d] : 0u;
             rank[i] = before + __popc(peers & lt);
@@ -330,7 +460,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const KT *__restrict_
             __syncwarp();
         }
         __syncthreads();
-        // per digit: exclusive over warps, block count
+        // per digit: exclusive over warps, block count, publish the aggregate
         unsigned cnt = 0;
 #pragma unroll
         for (int w = 0; w < 8; w++) {
@@ -339,50 +469,57 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const KT *__restrict_
             cnt += c;
         }
         unsigned long long *my = lb + (size_t)tile * 256 + t;
-        if (tile == 0) st_relaxed(my, pack(tag, kFlagInc, cnt));
-        else st_relaxed(my, pack(tag, kFlagAgg, cnt));
-        // block-exclusive scan of cnt over digits
-        {
+        st_relaxed(my, pack(tag, tile == 0 ? kFlagInc : kFlagAgg, cnt));
+        {  // block-exclusive scan of cnt over digits
             unsigned x = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= (unsigned)o) x += y;
             }
-            __shared__ unsigned s_ws2[8];
-            if (lane == 31) s_ws2[wid] = x;
+            if (lane == 31) s_misc[8 + wid] = x;
             __syncthreads();
             unsigned add = 0;
-            for (unsigned w = 0; w < wid; w++) add += s_ws2[w];
+            for (unsigned w = 0; w < wid; w++) add += s_misc[8 + w];
             s_doff[t] = x - cnt + add;
         }
-        // look-back for digit t
-        unsigned excl = 0;
-        if (tile > 0) {
-            int j = (int)tile - 1;
-            while (j >= 0) {
-                const unsigned long long e = ld_relaxed(lb + (size_t)j * 256 + t);
-                const unsigned hi = (unsigned)(e >> 32);
-                const unsigned flag = ((hi >> 2) == tag) ? (hi & 3u) : 0u;
-                if (flag == 0) continue;
-                excl += (unsigned)e;
-                if (flag == kFlagInc) break;
-                j--;
-            }
-            st_relaxed(my, pack(tag, kFlagInc, excl + cnt));
-        }
-        s_glob[t] = (int)(s_hex[t] + excl) - (int)s_doff[t];
         __syncthreads();
-        // scatter into smem in block-sorted order
+        // keys into shared memory at their block-sorted position
 #pragma unroll
         for (int i = 0; i < kSortItems; i++) {
-            const unsigned d = dig[i];
-            if (d < 256u) {
+            if (wbase + 32u * i < n) {
+                const unsigned d = (unsigned)((key[i] >> shift) & mask);
                 const unsigned pos = s_doff[d] + wh[d] + rank[i];
                 s_k[pos] = key[i];
                 s_v[pos] = val[i];
             }
         }
+        // look-back for digit t, kLookWin predecessors per round trip
+        unsigned excl = 0;
+        if (tile > 0) {
+            int j = (int)tile - 1;
+            while (true) {
+                unsigned long long e[kLookWin];
+#pragma unroll
+                for (int k = 0; k < kLookWin; k++)
+                    e[k] = (j - k >= 0) ? ld_relaxed(lb + (size_t)(j - k) * 256 + t) : pack(tag, kFlagInc, 0u);
+                unsigned acc = 0;
+                int k = 0;
+                bool found = false;
+                for (; k < kLookWin; k++) {
+                    const unsigned hi = (unsigned)(e[k] >> 32);
+                    const unsigned flag = ((hi >> 2) == tag) ? (hi & 3u) : 0u;
+                    if (flag == 0) break;
+                    acc += (unsigned)e[k];
+                    if (flag == kFlagInc) { found = true; break; }
+                }
+                excl += acc;
+                if (found) break;
+                j -= k;  // retry from the first entry that was not ready
+            }
+            st_relaxed(my, pack(tag, kFlagInc, excl + cnt));
+        }
+        s_glob[t] = (int)(s_hex[t] + excl) - (int)s_doff[t];
         __syncthreads();
         const unsigned nt = min((unsigned)kSortTile, n - base);
         for (unsigned k = t; k < nt; k += kSortThreads) {
@@ -395,24 +532,60 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const KT *__restrict_
     }
 }
 
-template <typename KT>
-static size_t onesweep_smem() {
-    return (8 * 256 + 256 * 3 + 4) * sizeof(unsigned) + kSortTile * (sizeof(KT) + sizeof(uint32_t));
+// ranges[tile] = [first, last + 1) over the sorted u16 tile keys; 8 keys per
+// thread through one 16-byte load (the buffer base is 256-byte aligned).
+__global__ void __launch_bounds__(256) k_ranges16(const uint16_t *__restrict__ keys, const unsigned *n_ptr,
+                                                  uint2 *ranges, const DevState *st) {
+    if (st->overflow) return;
+    const unsigned n = *n_ptr;
+    const unsigned chunks = (n + 7) / 8;
+    for (unsigned c = blockIdx.x * blockDim.x + threadIdx.x; c < chunks; c += gridDim.x * blockDim.x) {
+        const unsigned i0 = c * 8;
+        uint16_t k[8];
+        if (i0 + 8 <= n) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4 *>(keys) + c);
+            const uint16_t *p = reinterpret_cast<const uint16_t *>(&q);
+#pragma unroll
+            for (int j = 0; j < 8; j++) k[j] = p[j];
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++) k[j] = i0 + j < n ? keys[i0 + j] : 0;
+        }
+        const unsigned prev = i0 > 0 ? keys[i0 - 1] : 0xFFFFFFFFu;
+        const unsigned next = i0 + 8 < n ? keys[i0 + 8] : 0xFFFFFFFFu;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            if (i0 + j >= n) break;
+            const unsigned cur = k[j];
+            const unsigned pv = j ? (unsigned)k[j - 1] : prev;
+            const unsigned nx = (j < 7 && i0 + j + 1 < n) ? (unsigned)k[j + 1] : (i0 + j + 1 < n ? next : 0xFFFFFFFFu);
+            if (cur != pv) ranges[cur].x = i0 + j;
+            if (cur != nx) ranges[cur].y = i0 + j + 1;
+        }
+    }
 }
 
-// ranges[tile] = [first, last + 1) over the sorted keys
-template <typename KT>
-__global__ void k_ranges(const KT *__restrict__ keys, const unsigned *n_ptr, int shift, uint2 *ranges,
-                         const DevState *st) {
+__global__ void k_ranges64(const unsigned long long *__restrict__ keys, const unsigned *n_ptr, uint2 *ranges,
+                           const DevState *st) {
     if (st->overflow) return;
     const unsigned n = *n_ptr;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const unsigned tl = (unsigned)(keys[i] >> shift);
-        const unsigned prev = i > 0 ? (unsigned)(keys[i - 1] >> shift) : 0xFFFFFFFFu;
-        const unsigned next = i + 1 < n ? (unsigned)(keys[i + 1] >> shift) : 0xFFFFFFFFu;
+        const unsigned tl = (unsigned)(keys[i] >> 32);
+        const unsigned prev = i > 0 ? (unsigned)(keys[i - 1] >> 32) : 0xFFFFFFFFu;
+        const unsigned next = i + 1 < n ? (unsigned)(keys[i + 1] >> 32) : 0xFFFFFFFFu;
         if (tl != prev) ranges[tl].x = i;
         if (tl != next) ranges[tl].y = i + 1;
     }
+}
+
+template <typename KT>
+static size_t onesweep_smem() {
+    return (8 * 256 + 256 * 3 + 16) * sizeof(unsigned) + kSortTile * (sizeof(KT) + sizeof(uint32_t));
+}
+
+template <bool FULL>
+static size_t dup_smem() {
+    return DupCfg<FULL>::CAP * (sizeof(typename DupCfg<FULL>::Key) + sizeof(uint32_t));
 }
 
 static int bits_for(int64_t tiles) {
@@ -425,9 +598,8 @@ template <typename KT>
 static void onesweep_pass(Buffers &b, const KT *kin, const uint32_t *vin, KT *kout, uint32_t *vout,
                           const unsigned *n_ptr, int shift, int bits, int hist_row, int slot, int grid,
                           cudaStream_t s) {
-    const size_t sm = onesweep_smem<KT>();
-    k_onesweep<KT><<<grid, kSortThreads, sm, s>>>(kin, vin, kout, vout, n_ptr, shift, bits,
-                                                  &b.st->hist[hist_row][0], slot, b.lookback, b.st);
+    k_onesweep<KT><<<grid, kSortThreads, onesweep_smem<KT>(), s>>>(kin, vin, kout, vout, n_ptr, shift, bits,
+                                                                  &b.st->hist[hist_row][0], slot, b.lookback, b.st);
 }
 
 static int sort_grid(int64_t max_items, int sm_count, int per_sm) {
@@ -435,80 +607,87 @@ static int sort_grid(int64_t max_items, int sm_count, int per_sm) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count * per_sm));
 }
 
+static void set_attrs() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(k_onesweep<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)onesweep_smem<uint16_t>());
+    cudaFuncSetAttribute(k_onesweep<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)onesweep_smem<uint32_t>());
+    cudaFuncSetAttribute(k_onesweep<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)onesweep_smem<unsigned long long>());
+    cudaFuncSetAttribute(k_duplicate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dup_smem<false>());
+    cudaFuncSetAttribute(k_duplicate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dup_smem<true>());
+    done = true;
+}
+
 int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam, int sort_mode, cudaStream_t s,
                int sm_count) {
     (void)N; (void)F;
+    set_attrs();
     int launches = 0;
     const int64_t tiles = (int64_t)cam.tiles_x * cam.tiles_y;
     const int tb = bits_for(tiles);
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaFuncSetAttribute(k_onesweep<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)onesweep_smem<uint16_t>());
-        cudaFuncSetAttribute(k_onesweep<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)onesweep_smem<uint32_t>());
-        cudaFuncSetAttribute(k_onesweep<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)onesweep_smem<unsigned long long>());
-        attr_done = true;
+    const bool full = sort_mode == 1;
+    cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * (size_t)tiles, s);
+    const int scan_grid =
+        (int)std::max<int64_t>(1, std::min<int64_t>((P + kScanTile - 1) / kScanTile, (int64_t)sm_count * 8));
+    if (P > 0) {
+        if (full)
+            k_compact<true><<<scan_grid, kScanThreads, 0, s>>>(P, b.touched, b.dkey, b.rect, cam.tiles_x, tb, b.pk[0],
+                                                               b.pv[0], b.lookback, b.st);
+        else
+            k_compact<false><<<scan_grid, kScanThreads, 0, s>>>(P, b.touched, b.dkey, b.rect, cam.tiles_x, tb, b.pk[0],
+                                                                b.pv[0], b.lookback, b.st);
+        launches++;
     }
-    cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * tiles, s);
-    const int scan_grid = (int)std::max<int64_t>(1, std::min<int64_t>((P + kScanTile - 1) / kScanTile, (int64_t)sm_count * 8));
-    if (sort_mode == 0) {
-        // 1. compact visible primitives + depth histograms
-        if (P > 0) {
-            k_compact<<<scan_grid, kScanThreads, 0, s>>>(P, b.touched, b.dkey, b.pk[0], b.pv[0], b.lookback, b.st);
-            launches++;
-        }
-        // 2. four stable 8-bit passes on the depth key
-        const int g1 = sort_grid(P, sm_count, 3);
+    k_tile_lo_hist<<<1, 256, 0, s>>>(b.st);
+    launches++;
+    int slot = SLOT_PASS0;
+    const int dgrid =
+        (int)std::max<int64_t>(1, std::min<int64_t>((P + kScanTile - 1) / kScanTile, (int64_t)sm_count * 4));
+    const int g2 = sort_grid(b.max_pairs, sm_count, 2);
+    int tc = 0;
+    if (!full) {
+        // depth sort of the visible primitives
+        const int g1 = sort_grid(P, sm_count, 2);
         int cur = 0;
-        for (int pass = 0; pass < 4; pass++) {
+        for (int pass = 0; pass < 4; pass++, slot++) {
             onesweep_pass<uint32_t>(b, b.pk[cur], b.pv[cur], b.pk[cur ^ 1], b.pv[cur ^ 1], &b.st->n_vis, 8 * pass, 8,
-                                    HIST_DEPTH0 + pass, SLOT_DEPTH0 + pass, g1, s);
+                                    HIST_DEPTH0 + pass, slot, g1, s);
             cur ^= 1;
             launches++;
         }
-        // 3. scan tiles_touched in depth order + duplicate (u16 tile, id)
-        k_duplicate<false><<<scan_grid, kScanThreads, 0, s>>>(P, b.pv[cur], b.touched, b.rect, b.dkey, cam.tiles_x,
-                                                              tb, b.max_pairs, b.tk[0], b.tv[0], b.lookback, b.st);
+        k_duplicate<false><<<dgrid, kScanThreads, dup_smem<false>(), s>>>(b.pv[cur], b.touched, b.rect, b.dkey,
+                                                                          cam.tiles_x, b.max_pairs, b.tk[0], b.tv[0],
+                                                                          b.lookback, b.st);
         launches++;
-        // 4. stable passes on the tile id
-        const int g2 = sort_grid(b.max_pairs, sm_count, 4);
-        int tc = 0;
-        for (int pass = 0, sh = 0; sh < tb; pass++, sh += 8) {
+        for (int pass = 0, sh = 0; sh < tb; pass++, sh += 8, slot++) {
             onesweep_pass<uint16_t>(b, (const uint16_t *)b.tk[tc], b.tv[tc], (uint16_t *)b.tk[tc ^ 1], b.tv[tc ^ 1],
-                                    &b.st->K, sh, std::min(8, tb - sh), HIST_TILE0 + pass, SLOT_TILE0 + pass, g2, s);
+                                    &b.st->K, sh, std::min(8, tb - sh), HIST_TILE0 + pass, slot, g2, s);
             tc ^= 1;
             launches++;
         }
-        b.sorted_keys = b.tk[tc];
-        b.sorted_vals = b.tv[tc];
         b.key_bytes = 2;
-        k_ranges<uint16_t><<<sm_count * 4, 256, 0, s>>>((const uint16_t *)b.tk[tc], &b.st->K, 0, b.ranges, b.st);
+        k_ranges16<<<sm_count * 4, 256, 0, s>>>((const uint16_t *)b.tk[tc], &b.st->K, b.ranges, b.st);
         launches++;
     } else {
-        // 1. scan tiles_touched in id order + duplicate 64-bit keys (all 6 digit histograms)
-        if (P > 0) {
-            k_duplicate<true><<<scan_grid, kScanThreads, 0, s>>>(P, nullptr, b.touched, b.rect, b.dkey, cam.tiles_x, tb,
-                                                                 b.max_pairs, b.tk[0], b.tv[0], b.lookback, b.st);
-            launches++;
-        }
-        const int g2 = sort_grid(b.max_pairs, sm_count, 3);
-        int tc = 0;
+        k_duplicate<true><<<dgrid, kScanThreads, dup_smem<true>(), s>>>(b.pv[0], b.touched, b.rect, b.dkey, cam.tiles_x,
+                                                                        b.max_pairs, b.tk[0], b.tv[0], b.lookback, b.st);
+        launches++;
         const int total_bits = 32 + tb;
-        for (int pass = 0, sh = 0; sh < total_bits; pass++, sh += 8) {
+        for (int pass = 0, sh = 0; sh < total_bits; pass++, sh += 8, slot++) {
             onesweep_pass<unsigned long long>(b, (const unsigned long long *)b.tk[tc], b.tv[tc],
                                               (unsigned long long *)b.tk[tc ^ 1], b.tv[tc ^ 1], &b.st->K, sh,
-                                              std::min(8, total_bits - sh), pass, SLOT_FULL0 + pass, g2, s);
+                                              std::min(8, total_bits - sh), pass, slot, g2, s);
             tc ^= 1;
             launches++;
         }
-        b.sorted_keys = b.tk[tc];
-        b.sorted_vals = b.tv[tc];
         b.key_bytes = 8;
-        k_ranges<unsigned long long><<<sm_count * 4, 256, 0, s>>>((const unsigned long long *)b.tk[tc], &b.st->K, 32,
-                                                                  b.ranges, b.st);
+        k_ranges64<<<sm_count * 4, 256, 0, s>>>((const unsigned long long *)b.tk[tc], &b.st->K, b.ranges, b.st);
         launches++;
     }
-    return launches + 1;  // + the ranges memset
+    b.sorted_keys = b.tk[tc];
+    b.sorted_vals = b.tv[tc];
+    return launches;  // kernels only (the ranges memset is not counted)
 }
 
 // ---- debug / stats ------------------------------------------------------------

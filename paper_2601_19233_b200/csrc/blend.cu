@@ -100,53 +100,142 @@ __device__ __forceinline__ void tri_colour(const TriRecord &r, const long long E
     }
 }
 
-__global__ void __launch_bounds__(kBlendThreads) k_blend(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ vals,
-                                                         const GaussRecord *__restrict__ grec,
-                                                         const TriRecord *__restrict__ trec, TexView tv, unsigned F,
-                                                         int W, int H, int tiles_x, BlendParams bp,
-                                                         float4 *__restrict__ out, const DevState *st) {
+// Per-warp culling of a staged entry (exact, never drops a fragment).
+// Warp w owns the 8x4 sub-tile (w & 1, w >> 1) of the 16x16 tile.  Bit w of the
+// mask is cleared only when no pixel of that sub-tile can hold the fragment:
+//   triangle: its snapped integer bbox misses the sub-tile's 1/256-px extent;
+//   Gaussian: the sub-tile's pixel centres lie outside the bbox of the exact
+//   ellipse {d : Q(d) <= q_max (1 + 0.02)} of the fp32 conic Q, padded by
+//   1% + 0.01 px.  Only for cond(Q) <= ~1000, where the fp32 evaluation of q
+//   (10 roundings, cancellation factor <= 2(cond + 1)) errs by < 1.3e-3 q, so a
+//   pixel outside that ellipse cannot satisfy the N6 test q <= q_max.  Other
+//   conics (needles, NaN) keep all bits set.
+__device__ __forceinline__ unsigned gauss_warp_mask(const float4 &a, const float4 &b, float ox, float oy) {
+    const float ca = b.x, cb = b.y, cc = b.z;
+    const float det = ca * cc - cb * cb, sum = ca + cc;
+    if (!(det > 0.f && sum * sum <= 1000.f * det)) return 0xFFu;
+    const float ex = sqrtf(a.z * cc / det) * 1.01f + 0.01f;
+    const float ey = sqrtf(a.z * ca / det) * 1.01f + 0.01f;
+    if (!(ex < 1e30f && ey < 1e30f)) return 0xFFu;
+    const float xlo = a.x - ex, xhi = a.x + ex, ylo = a.y - ey, yhi = a.y + ey;
+    unsigned m = 0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+        const float x0 = ox + (float)((w & 1) * 8) + 0.5f, y0 = oy + (float)((w >> 1) * 4) + 0.5f;
+        if (xhi >= x0 && xlo <= x0 + 7.f && yhi >= y0 && ylo <= y0 + 3.f) m |= 1u << w;
+    }
+    return m;
+}
+
+__device__ __forceinline__ unsigned tri_warp_mask(const int4 &q0, const int4 &q1, int tx, int ty) {
+    const int mnx = min(q0.x, min(q0.z, q1.x)), mxx = max(q0.x, max(q0.z, q1.x));
+    const int mny = min(q0.y, min(q0.w, q1.y)), mxy = max(q0.y, max(q0.w, q1.y));
+    unsigned m = 0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+        const int x0 = 256 * (tx * kTile + (w & 1) * 8), y0 = 256 * (ty * kTile + (w >> 1) * 4);
+        if (mxx >= x0 && mnx <= x0 + 256 * 8 - 1 && mxy >= y0 && mny <= y0 + 256 * 4 - 1) m |= 1u << w;
+    }
+    return m;
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2 *__restrict__ ranges,
+                                                            const uint32_t *__restrict__ vals,
+                                                            const GaussRecord *__restrict__ grec,
+                                                            const TriRecord *__restrict__ trec, TexView tv,
+                                                            unsigned F, int W, int H, int tiles_x, BlendParams bp,
+                                                            float4 *__restrict__ out, DevState *st) {
     if (st->overflow) return;
+    unsigned long long w_gt = 0, w_gf = 0, w_tt = 0, w_tf = 0;  // COUNT only
     __shared__ float4 s_a[kBlendThreads];  // u, v, q_max, o
     __shared__ float4 s_b[kBlendThreads];  // ca, 2 cb, cc, -
     __shared__ float4 s_c[kBlendThreads];  // r, g, b, -
     __shared__ unsigned s_id[kBlendThreads];
+    __shared__ unsigned char s_mask[kBlendThreads];
+    __shared__ unsigned char s_list[kBlendThreads / 32][kBlendThreads];
 
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
+    const int x = tx * kTile + (warp & 1) * 8 + (lane & 7), y = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
     const bool inside = x < W && y < H;
     const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+    const float tox = (float)(tx * kTile), toy = (float)(ty * kTile);
     const uint2 rg = ranges[tile];
+    const unsigned lt = (1u << lane) - 1u;
 
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, T = 1.f, Te = 1.f;
     float t0 = 1.f, t1 = 1.f, t2 = 1.f, t3 = 1.f;
     bool open = false, done = !inside;
 
-    for (unsigned base = rg.x; base < rg.y; base += kBlendThreads) {
-        if (__syncthreads_count(done) == kBlendThreads) break;
-        const unsigned i = base + threadIdx.x;
+    // software pipeline: the next batch's id and record are in flight while this one is blended
+    unsigned nid = 0xFFFFFFFFu;
+    float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na, nc = na;
+    auto fetch = [&](unsigned i) {
+        nid = 0xFFFFFFFFu;
         if (i < rg.y) {
-            const unsigned id = __ldg(vals + i);
-            s_id[threadIdx.x] = id;
-            if (id >= F) {
-                const GaussRecord *g = grec + (id - F);
-                const float4 a = __ldg(&g->a), bb = __ldg(&g->b), c = __ldg(&g->c);
-                s_a[threadIdx.x] = a;
-                s_b[threadIdx.x] = make_float4(bb.x, bb.y + bb.y, bb.z, 0.f);
-                s_c[threadIdx.x] = c;
+            nid = __ldg(vals + i);
+            if (nid >= F) {
+                const GaussRecord *g = grec + (nid - F);
+                na = __ldg(&g->a); nb = __ldg(&g->b); nc = __ldg(&g->c);
+            } else {
+                const int4 *q = reinterpret_cast<const int4 *>(trec + nid);
+                const int4 q0 = __ldg(q), q1 = __ldg(q + 1);
+                na = make_float4(__int_as_float(q0.x), __int_as_float(q0.y), __int_as_float(q0.z), __int_as_float(q0.w));
+                nb = make_float4(__int_as_float(q1.x), __int_as_float(q1.y), __int_as_float(q1.z), __int_as_float(q1.w));
             }
         }
+    };
+    fetch(rg.x + threadIdx.x);
+
+    for (unsigned base = rg.x; base < rg.y; base += kBlendThreads) {
+        if (__syncthreads_count(done) == kBlendThreads) break;
+        // commit the prefetched entry to shared memory with its warp mask
+        {
+            unsigned m = 0;
+            if (nid != 0xFFFFFFFFu) {
+                s_id[threadIdx.x] = nid;
+                if (nid >= F) {
+                    s_a[threadIdx.x] = na;
+                    s_b[threadIdx.x] = make_float4(nb.x, nb.y + nb.y, nb.z, 0.f);
+                    s_c[threadIdx.x] = nc;
+                    m = gauss_warp_mask(na, nb, tox, toy);
+                } else {
+                    const int4 q0 = make_int4(__float_as_int(na.x), __float_as_int(na.y), __float_as_int(na.z), __float_as_int(na.w));
+                    const int4 q1 = make_int4(__float_as_int(nb.x), __float_as_int(nb.y), __float_as_int(nb.z), __float_as_int(nb.w));
+                    m = tri_warp_mask(q0, q1, tx, ty);
+                }
+            }
+            s_mask[threadIdx.x] = (unsigned char)m;
+        }
         __syncthreads();
-        if (done) continue;
+        fetch(base + kBlendThreads + threadIdx.x);
+        if (__all_sync(0xffffffffu, done)) continue;
+        // this warp's relevant entries, in list order
         const unsigned n = min((unsigned)kBlendThreads, rg.y - base);
-        for (unsigned j = 0; j < n; j++) {
+        unsigned cnt = 0;
+        for (unsigned c = 0; c < n; c += 32) {
+            const unsigned j = c + lane;
+            const bool rel = j < n && ((s_mask[j] >> warp) & 1u);
+            const unsigned bal = __ballot_sync(0xffffffffu, rel);
+            if (rel) s_list[warp][cnt + __popc(bal & lt)] = (unsigned char)j;
+            cnt += __popc(bal);
+        }
+        __syncwarp();
+        for (unsigned k = 0; k < cnt; k++) {
+            if ((k & 7) == 0 && __all_sync(0xffffffffu, done)) break;
+            if (done) continue;
+            const unsigned j = s_list[warp][k];
             const unsigned id = s_id[j];
             if (id >= F) {
+                if (COUNT) w_gt++;
                 const float4 a = s_a[j];
                 const float dx = __fsub_rn(px, a.x), dy = __fsub_rn(py, a.y);
                 const float4 b = s_b[j];
                 const float q = __fmaf_rn(b.x, __fmul_rn(dx, dx), __fmaf_rn(b.z, __fmul_rn(dy, dy), __fmul_rn(b.y, __fmul_rn(dx, dy))));
                 if (!(q <= a.z)) continue;
+                if (COUNT) w_gf++;
                 const float al = fminf(bp.alpha_max, a.w * __expf(-0.5f * q));
                 if (open) {
                     T = Te * ((t0 + t1) + (t2 + t3)) * 0.25f;
@@ -156,14 +245,16 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint2 *__restrict
                 const float w = T * al;
                 C0 += w * c.x; C1 += w * c.y; C2 += w * c.z;
                 T -= w;
-                if (T < bp.t_eps) { done = true; break; }
+                if (T < bp.t_eps) done = true;
             } else {
                 const TriRecord &r = trec[id];
                 const int4 q0 = r.q0, q1 = r.q1;
                 const int X[3] = {q0.x, q0.z, q1.x}, Y[3] = {q0.y, q0.w, q1.y};
                 long long Ec[3];
+                if (COUNT) w_tt++;
                 const unsigned m = coverage(X, Y, x, y, Ec);
                 if (!m) continue;
+                if (COUNT) w_tf++;
                 TriRecord rr;
                 rr.q0 = q0; rr.q1 = q1; rr.q2 = r.q2; rr.q3 = r.q3; rr.q4 = r.q4; rr.q5 = r.q5;
                 float rgb[3];
@@ -177,16 +268,26 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint2 *__restrict
                 const float O = (((m & 1) ? t0 : 0.f) + ((m & 2) ? t1 : 0.f) + ((m & 4) ? t2 : 0.f) + ((m & 8) ? t3 : 0.f)) * 0.25f;
                 const float w = Te * O * al;
                 C0 += w * rgb[0]; C1 += w * rgb[1]; C2 += w * rgb[2];
-                const float k = 1.f - al;
-                if (m & 1) t0 *= k;
-                if (m & 2) t1 *= k;
-                if (m & 4) t2 *= k;
-                if (m & 8) t3 *= k;
-                if (Te * ((t0 + t1) + (t2 + t3)) * 0.25f < bp.t_eps) { done = true; break; }
+                const float kk = 1.f - al;
+                if (m & 1) t0 *= kk;
+                if (m & 2) t1 *= kk;
+                if (m & 4) t2 *= kk;
+                if (m & 8) t3 *= kk;
+                if (Te * ((t0 + t1) + (t2 + t3)) * 0.25f < bp.t_eps) done = true;
             }
         }
     }
     if (open) T = Te * ((t0 + t1) + (t2 + t3)) * 0.25f;
+    if (COUNT) {
+        unsigned long long v[4] = {w_gt, w_gf, w_tt, w_tf};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            unsigned long long xs = v[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+            if (lane == 0 && xs) atomicAdd(&st->work[k], xs);
+        }
+    }
     if (inside) {
         const float s = T * bp.bg_alpha;
         out[(size_t)y * W + x] = make_float4(C0 + s * bp.bg[0], C1 + s * bp.bg[1], C2 + s * bp.bg[2], T);
@@ -194,12 +295,16 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint2 *__restrict
 }
 
 int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, const CamParams &cam,
-                 const BlendParams &bp, float *out, cudaStream_t s) {
+                 const BlendParams &bp, float *out, cudaStream_t s, bool count_work) {
     (void)g;
     const int tiles = cam.tiles_x * cam.tiles_y;
     TexView tv{reinterpret_cast<const uchar4 *>(m.tex), m.tw, m.th};
-    k_blend<<<tiles, kBlendThreads, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv, (unsigned)m.F, cam.W, cam.H,
-                                            cam.tiles_x, bp, reinterpret_cast<float4 *>(out), b.st);
+    if (count_work)
+        k_blend<true><<<tiles, kBlendThreads, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv, (unsigned)m.F, cam.W,
+                                                      cam.H, cam.tiles_x, bp, reinterpret_cast<float4 *>(out), b.st);
+    else
+        k_blend<false><<<tiles, kBlendThreads, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv, (unsigned)m.F, cam.W,
+                                                       cam.H, cam.tiles_x, bp, reinterpret_cast<float4 *>(out), b.st);
     return 1;
 }
 

@@ -24,6 +24,9 @@ struct DevState {
     unsigned int ctr[16];       // dynamic tile counters of the scans / sort passes
     unsigned int hist[kMaxPasses][256];
     unsigned int max_tile_pairs, max_tile_id;
+    unsigned long long work[4];  // blend work counters (counting variant only)
+    unsigned int tdlo[257];      // difference array of the low tile-digit histogram
+    unsigned int tdlo_all;       // full 256-cycles of low tile digits
 };
 
 // Camera + the per-frame constants every stage needs.
@@ -101,7 +104,7 @@ int launch_setup_triangles(const MeshInput &m, const CamParams &cam, const Buffe
 int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam, int sort_mode, cudaStream_t s,
                int sm_count);
 int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, const CamParams &cam,
-                 const BlendParams &bp, float *out, cudaStream_t s);
+                 const BlendParams &bp, float *out, cudaStream_t s, bool count_work = false);
 int launch_tile_stats(const Buffers &b, int tiles, cudaStream_t s);
 int launch_full_keys(const Buffers &b, uint64_t *keys, cudaStream_t s);
 

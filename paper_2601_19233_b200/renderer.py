@@ -169,6 +169,14 @@ class Renderer:
         self._check(self.L.unimgs_render(self._h, C.c_void_p(out.data_ptr()), _stream_handle(stream)))
         return out
 
+    def render_counted(self, out: Optional[torch.Tensor] = None, stream=None):
+        """Render through the work-counting kernel variant; returns (out, work dict)."""
+        if out is None:
+            out = torch.empty((self._cam.height, self._cam.width, 4), dtype=torch.float32, device="cuda")
+        w = (C.c_int64 * 4)()
+        self._check(self.L.unimgs_render_counted(self._h, C.c_void_p(out.data_ptr()), w, _stream_handle(stream)))
+        return out, dict(gauss_tests=w[0], gauss_frags=w[1], tri_tests=w[2], tri_frags=w[3])
+
     def render_view(self, scene: DeviceScene, cam: SceneCamera, out=None, stream=None) -> torch.Tensor:
         self.preprocess(scene, cam, stream)
         self.bin(stream)
