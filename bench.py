@@ -315,8 +315,11 @@ def run_ours(a, rank, world, local_rank):
         return
     # ---- roofline of the dominant kernel (blend, ALU/issue-bound) -----------------
     n_blend = len(timed_views)
-    ops = (work["gauss_tests"] * OPS_GAUSS_TEST + work["gauss_frags"] * OPS_GAUSS_FRAG
-           + work["tri_tests"] * OPS_TRI_TEST + work["tri_frags"] * OPS_TRI_FRAG) / n_blend
+    # algorithmic work of the blend = every fragment a pixel blends before it terminates,
+    # each evaluated once (membership test + blend).  Tests of list entries that turn out
+    # not to be fragments of the pixel are tiling overhead, reported but not credited.
+    ops = (work["gauss_frags"] * (OPS_GAUSS_TEST + OPS_GAUSS_FRAG)
+           + work["tri_frags"] * (OPS_TRI_TEST + OPS_TRI_FRAG)) / n_blend
     import torch as _t
     props = _t.cuda.get_device_properties(dev)
     sm_count = props.multi_processor_count

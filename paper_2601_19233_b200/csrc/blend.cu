@@ -1,10 +1,11 @@
 // blend.cu -- B8: the unified single-pass anti-aliased blend (§3.2).
 //
-// One CTA per 16x16 tile, one thread per pixel.  The tile's sorted list
-// (unified ids, (tile, depth, id) order) is staged through shared memory in
-// batches of 256 entries; Gaussian records are gathered with 16-byte loads
-// into SoA shared arrays, triangle entries are resolved from their 96-byte
-// setup record (broadcast loads: every lane reads the same address).
+// One CTA per 16x16 tile, one pixel per thread, 8 warps that each walk the
+// tile's sorted list (unified ids, (tile, depth, id) order) independently:
+// records are gathered with 16-byte loads, culled exactly against the warp's
+// 8x4 sub-tile, packed into a per-warp shared buffer and blended in list
+// order; triangle entries are resolved from their 96-byte setup record
+// (broadcast loads: every lane reads the same address).
 //
 // Per pixel (state machine of DESIGN.md §2 / the oracle):
 //   Gaussian fragment  iff q <= q_max (N6, bit-exact with the oracle):
@@ -14,8 +15,8 @@
 //       edge functions, top-left rule, D3D 4x pattern; N7, R10-R11):
 //       open an entity if none (T_e = T, t_j = 1; Eq.7), O = sum_j m_j t_j / 4
 //       (Eq.8), C += T_e O alpha c (Eq.9), t_j *= 1 - m_j alpha (Eq.7)
-//   stop once T_eff < t_eps (blend-then-test, R16); the block exits when
-//   every pixel has stopped (__syncthreads_count).
+//   stop once T_eff < t_eps (blend-then-test, R16); a warp exits when all of
+//   its pixels have stopped.
 //   out = (C + T bg_alpha bg, T) with the exit T of an open entity (R3, R5).
 // Triangle colour: perspective-correct barycentrics at the pixel centre in
 // fp64 (lambda_k ~ E_k z_i z_j, exact products), manual fp32 bilinear texture.
@@ -100,45 +101,40 @@ __device__ __forceinline__ void tri_colour(const TriRecord &r, const long long E
     }
 }
 
-// Per-warp culling of a staged entry (exact, never drops a fragment).
-// Warp w owns the 8x4 sub-tile (w & 1, w >> 1) of the 16x16 tile.  Bit w of the
-// mask is cleared only when no pixel of that sub-tile can hold the fragment:
+// Exact per-warp culling (never drops a fragment).  Warp w owns the 8x4
+// sub-tile (w & 1, w >> 1) of the 16x16 tile; an entry is skipped by the warp
+// only when no pixel of its sub-tile can hold the fragment:
 //   triangle: its snapped integer bbox misses the sub-tile's 1/256-px extent;
 //   Gaussian: the sub-tile's pixel centres lie outside the bbox of the exact
 //   ellipse {d : Q(d) <= q_max (1 + 0.02)} of the fp32 conic Q, padded by
 //   1% + 0.01 px.  Only for cond(Q) <= ~1000, where the fp32 evaluation of q
 //   (10 roundings, cancellation factor <= 2(cond + 1)) errs by < 1.3e-3 q, so a
 //   pixel outside that ellipse cannot satisfy the N6 test q <= q_max.  Other
-//   conics (needles, NaN) keep all bits set.
-__device__ __forceinline__ unsigned gauss_warp_mask(const float4 &a, const float4 &b, float ox, float oy) {
+//   conics (needles, NaN) are never skipped.
+__device__ __forceinline__ bool gauss_touches(const float4 &a, const float4 &b, float rx0, float ry0) {
     const float ca = b.x, cb = b.y, cc = b.z;
     const float det = ca * cc - cb * cb, sum = ca + cc;
-    if (!(det > 0.f && sum * sum <= 1000.f * det)) return 0xFFu;
+    if (!(det > 0.f && sum * sum <= 1000.f * det)) return true;
     const float ex = sqrtf(a.z * cc / det) * 1.01f + 0.01f;
     const float ey = sqrtf(a.z * ca / det) * 1.01f + 0.01f;
-    if (!(ex < 1e30f && ey < 1e30f)) return 0xFFu;
-    const float xlo = a.x - ex, xhi = a.x + ex, ylo = a.y - ey, yhi = a.y + ey;
-    unsigned m = 0;
-#pragma unroll
-    for (int w = 0; w < 8; w++) {
-        const float x0 = ox + (float)((w & 1) * 8) + 0.5f, y0 = oy + (float)((w >> 1) * 4) + 0.5f;
-        if (xhi >= x0 && xlo <= x0 + 7.f && yhi >= y0 && ylo <= y0 + 3.f) m |= 1u << w;
-    }
-    return m;
+    if (!(ex < 1e30f && ey < 1e30f)) return true;
+    return a.x + ex >= rx0 && a.x - ex <= rx0 + 7.f && a.y + ey >= ry0 && a.y - ey <= ry0 + 3.f;
 }
 
-__device__ __forceinline__ unsigned tri_warp_mask(const int4 &q0, const int4 &q1, int tx, int ty) {
-    const int mnx = min(q0.x, min(q0.z, q1.x)), mxx = max(q0.x, max(q0.z, q1.x));
-    const int mny = min(q0.y, min(q0.w, q1.y)), mxy = max(q0.y, max(q0.w, q1.y));
-    unsigned m = 0;
-#pragma unroll
-    for (int w = 0; w < 8; w++) {
-        const int x0 = 256 * (tx * kTile + (w & 1) * 8), y0 = 256 * (ty * kTile + (w >> 1) * 4);
-        if (mxx >= x0 && mnx <= x0 + 256 * 8 - 1 && mxy >= y0 && mny <= y0 + 256 * 4 - 1) m |= 1u << w;
-    }
-    return m;
+__device__ __forceinline__ bool tri_touches(const float4 &a, const float4 &b, int Rx0, int Ry0) {
+    const int X0 = __float_as_int(a.x), Y0 = __float_as_int(a.y), X1 = __float_as_int(a.z), Y1 = __float_as_int(a.w);
+    const int X2 = __float_as_int(b.x), Y2 = __float_as_int(b.y);
+    const int mnx = min(X0, min(X1, X2)), mxx = max(X0, max(X1, X2));
+    const int mny = min(Y0, min(Y1, Y2)), mxy = max(Y0, max(Y1, Y2));
+    return mxx >= Rx0 && mnx <= Rx0 + 256 * 8 - 1 && mxy >= Ry0 && mny <= Ry0 + 256 * 4 - 1;
 }
 
+// One CTA per 16x16 tile, 8 independent warps, one pixel per lane.  Each warp
+// walks the whole tile list in chunks of 32 (lane l holds entry 32c + l; ids are
+// prefetched two chunks ahead and records one chunk ahead), keeps the entries
+// that touch its sub-tile (ballot), packs them into its own shared buffer and
+// blends them in list order with broadcast reads.  No block-wide barrier: a
+// warp stops as soon as all of its pixels have terminated.
 template <bool COUNT>
 __global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2 *__restrict__ ranges,
                                                             const uint32_t *__restrict__ vals,
@@ -148,134 +144,114 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2 *__restr
                                                             float4 *__restrict__ out, DevState *st) {
     if (st->overflow) return;
     unsigned long long w_gt = 0, w_gf = 0, w_tt = 0, w_tf = 0;  // COUNT only
-    __shared__ float4 s_a[kBlendThreads];  // u, v, q_max, o
-    __shared__ float4 s_b[kBlendThreads];  // ca, 2 cb, cc, -
-    __shared__ float4 s_c[kBlendThreads];  // r, g, b, -
-    __shared__ unsigned s_id[kBlendThreads];
-    __shared__ unsigned char s_mask[kBlendThreads];
-    __shared__ unsigned char s_list[kBlendThreads / 32][kBlendThreads];
+    __shared__ float4 s_buf[kBlendThreads / 32][32][3];  // per-warp packed entries: a, (ca, 2cb, cc, id), c
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int x = tx * kTile + (warp & 1) * 8 + (lane & 7), y = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+    const int sx0 = tx * kTile + (warp & 1) * 8, sy0 = ty * kTile + (warp >> 1) * 4;
+    const int x = sx0 + (lane & 7), y = sy0 + (lane >> 3);
     const bool inside = x < W && y < H;
     const float px = (float)x + 0.5f, py = (float)y + 0.5f;
-    const float tox = (float)(tx * kTile), toy = (float)(ty * kTile);
+    const float rx0 = (float)sx0 + 0.5f, ry0 = (float)sy0 + 0.5f;
+    const int Rx0 = 256 * sx0, Ry0 = 256 * sy0;
     const uint2 rg = ranges[tile];
     const unsigned lt = (1u << lane) - 1u;
+    float4(*buf)[3] = s_buf[warp];
 
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, T = 1.f, Te = 1.f;
     float t0 = 1.f, t1 = 1.f, t2 = 1.f, t3 = 1.f;
     bool open = false, done = !inside;
 
-    // software pipeline: the next batch's id and record are in flight while this one is blended
-    unsigned nid = 0xFFFFFFFFu;
+    // ids two chunks ahead, records one chunk ahead
+    unsigned id1 = rg.x + lane < rg.y ? __ldg(vals + rg.x + lane) : 0xFFFFFFFFu;
+    unsigned id2 = rg.x + 32 + lane < rg.y ? __ldg(vals + rg.x + 32 + lane) : 0xFFFFFFFFu;
     float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na, nc = na;
-    auto fetch = [&](unsigned i) {
-        nid = 0xFFFFFFFFu;
-        if (i < rg.y) {
-            nid = __ldg(vals + i);
-            if (nid >= F) {
-                const GaussRecord *g = grec + (nid - F);
-                na = __ldg(&g->a); nb = __ldg(&g->b); nc = __ldg(&g->c);
-            } else {
-                const int4 *q = reinterpret_cast<const int4 *>(trec + nid);
-                const int4 q0 = __ldg(q), q1 = __ldg(q + 1);
-                na = make_float4(__int_as_float(q0.x), __int_as_float(q0.y), __int_as_float(q0.z), __int_as_float(q0.w));
-                nb = make_float4(__int_as_float(q1.x), __int_as_float(q1.y), __int_as_float(q1.z), __int_as_float(q1.w));
-            }
+    auto fetch_rec = [&](unsigned id) {
+        if (id == 0xFFFFFFFFu) return;
+        if (id >= F) {
+            const GaussRecord *g = grec + (id - F);
+            na = __ldg(&g->a); nb = __ldg(&g->b); nc = __ldg(&g->c);
+        } else {
+            const int4 *q = reinterpret_cast<const int4 *>(trec + id);
+            const int4 q0 = __ldg(q), q1 = __ldg(q + 1);
+            na = make_float4(__int_as_float(q0.x), __int_as_float(q0.y), __int_as_float(q0.z), __int_as_float(q0.w));
+            nb = make_float4(__int_as_float(q1.x), __int_as_float(q1.y), __int_as_float(q1.z), __int_as_float(q1.w));
         }
     };
-    fetch(rg.x + threadIdx.x);
+    fetch_rec(id1);
 
-    for (unsigned base = rg.x; base < rg.y; base += kBlendThreads) {
-        if (__syncthreads_count(done) == kBlendThreads) break;
-        // commit the prefetched entry to shared memory with its warp mask
-        {
-            unsigned m = 0;
-            if (nid != 0xFFFFFFFFu) {
-                s_id[threadIdx.x] = nid;
-                if (nid >= F) {
-                    s_a[threadIdx.x] = na;
-                    s_b[threadIdx.x] = make_float4(nb.x, nb.y + nb.y, nb.z, 0.f);
-                    s_c[threadIdx.x] = nc;
-                    m = gauss_warp_mask(na, nb, tox, toy);
-                } else {
-                    const int4 q0 = make_int4(__float_as_int(na.x), __float_as_int(na.y), __float_as_int(na.z), __float_as_int(na.w));
-                    const int4 q1 = make_int4(__float_as_int(nb.x), __float_as_int(nb.y), __float_as_int(nb.z), __float_as_int(nb.w));
-                    m = tri_warp_mask(q0, q1, tx, ty);
-                }
-            }
-            s_mask[threadIdx.x] = (unsigned char)m;
-        }
-        __syncthreads();
-        fetch(base + kBlendThreads + threadIdx.x);
-        if (__all_sync(0xffffffffu, done)) continue;
-        // this warp's relevant entries, in list order
-        const unsigned n = min((unsigned)kBlendThreads, rg.y - base);
-        unsigned cnt = 0;
-        for (unsigned c = 0; c < n; c += 32) {
-            const unsigned j = c + lane;
-            const bool rel = j < n && ((s_mask[j] >> warp) & 1u);
-            const unsigned bal = __ballot_sync(0xffffffffu, rel);
-            if (rel) s_list[warp][cnt + __popc(bal & lt)] = (unsigned char)j;
-            cnt += __popc(bal);
+    for (unsigned base = rg.x; base < rg.y; base += 32) {
+        if (__all_sync(0xffffffffu, done)) break;
+        const unsigned id = id1;
+        const float4 a = na, b = nb, c = nc;
+        id1 = id2;
+        id2 = base + 64 + lane < rg.y ? __ldg(vals + base + 64 + lane) : 0xFFFFFFFFu;
+        fetch_rec(id1);
+        bool rel = false;
+        if (id != 0xFFFFFFFFu) rel = id >= F ? gauss_touches(a, b, rx0, ry0) : tri_touches(a, b, Rx0, Ry0);
+        const unsigned bal = __ballot_sync(0xffffffffu, rel);
+        if (rel) {
+            const unsigned slot = __popc(bal & lt);
+            buf[slot][0] = a;
+            buf[slot][1] = make_float4(b.x, b.y + b.y, b.z, __uint_as_float(id));
+            buf[slot][2] = c;
         }
         __syncwarp();
+        const unsigned cnt = __popc(bal);
         for (unsigned k = 0; k < cnt; k++) {
-            if ((k & 7) == 0 && __all_sync(0xffffffffu, done)) break;
-            if (done) continue;
-            const unsigned j = s_list[warp][k];
-            const unsigned id = s_id[j];
-            if (id >= F) {
-                if (COUNT) w_gt++;
-                const float4 a = s_a[j];
-                const float dx = __fsub_rn(px, a.x), dy = __fsub_rn(py, a.y);
-                const float4 b = s_b[j];
-                const float q = __fmaf_rn(b.x, __fmul_rn(dx, dx), __fmaf_rn(b.z, __fmul_rn(dy, dy), __fmul_rn(b.y, __fmul_rn(dx, dy))));
-                if (!(q <= a.z)) continue;
-                if (COUNT) w_gf++;
-                const float al = fminf(bp.alpha_max, a.w * __expf(-0.5f * q));
-                if (open) {
-                    T = Te * ((t0 + t1) + (t2 + t3)) * 0.25f;
-                    open = false;
+            const float4 eb = buf[k][1];
+            const unsigned eid = __float_as_uint(eb.w);
+            if (eid >= F) {
+                if (COUNT && !done) w_gt++;
+                const float4 ea = buf[k][0];
+                const float dx = __fsub_rn(px, ea.x), dy = __fsub_rn(py, ea.y);
+                const float q = __fmaf_rn(eb.x, __fmul_rn(dx, dx), __fmaf_rn(eb.z, __fmul_rn(dy, dy), __fmul_rn(eb.y, __fmul_rn(dx, dy))));
+                if (q <= ea.z && !done) {
+                    if (COUNT) w_gf++;
+                    const float al = fminf(bp.alpha_max, ea.w * __expf(-0.5f * q));
+                    if (open) {
+                        T = Te * ((t0 + t1) + (t2 + t3)) * 0.25f;
+                        open = false;
+                    }
+                    const float4 ec = buf[k][2];
+                    const float w = T * al;
+                    C0 += w * ec.x; C1 += w * ec.y; C2 += w * ec.z;
+                    T -= w;
+                    if (T < bp.t_eps) done = true;
                 }
-                const float4 c = s_c[j];
-                const float w = T * al;
-                C0 += w * c.x; C1 += w * c.y; C2 += w * c.z;
-                T -= w;
-                if (T < bp.t_eps) done = true;
-            } else {
-                const TriRecord &r = trec[id];
+            } else if (!done) {
+                const TriRecord &r = trec[eid];
                 const int4 q0 = r.q0, q1 = r.q1;
                 const int X[3] = {q0.x, q0.z, q1.x}, Y[3] = {q0.y, q0.w, q1.y};
                 long long Ec[3];
                 if (COUNT) w_tt++;
                 const unsigned m = coverage(X, Y, x, y, Ec);
-                if (!m) continue;
-                if (COUNT) w_tf++;
-                TriRecord rr;
-                rr.q0 = q0; rr.q1 = q1; rr.q2 = r.q2; rr.q3 = r.q3; rr.q4 = r.q4; rr.q5 = r.q5;
-                float rgb[3];
-                tri_colour(rr, Ec, tv, rgb);
-                const float al = __int_as_float(q1.w);
-                if (!open) {
-                    open = true;
-                    Te = T;
-                    t0 = t1 = t2 = t3 = 1.f;
+                if (m) {
+                    if (COUNT) w_tf++;
+                    TriRecord rr;
+                    rr.q0 = q0; rr.q1 = q1; rr.q2 = r.q2; rr.q3 = r.q3; rr.q4 = r.q4; rr.q5 = r.q5;
+                    float rgb[3];
+                    tri_colour(rr, Ec, tv, rgb);
+                    const float al = __int_as_float(q1.w);
+                    if (!open) {
+                        open = true;
+                        Te = T;
+                        t0 = t1 = t2 = t3 = 1.f;
+                    }
+                    const float O = (((m & 1) ? t0 : 0.f) + ((m & 2) ? t1 : 0.f) + ((m & 4) ? t2 : 0.f) + ((m & 8) ? t3 : 0.f)) * 0.25f;
+                    const float w = Te * O * al;
+                    C0 += w * rgb[0]; C1 += w * rgb[1]; C2 += w * rgb[2];
+                    const float kk = 1.f - al;
+                    if (m & 1) t0 *= kk;
+                    if (m & 2) t1 *= kk;
+                    if (m & 4) t2 *= kk;
+                    if (m & 8) t3 *= kk;
+                    if (Te * ((t0 + t1) + (t2 + t3)) * 0.25f < bp.t_eps) done = true;
                 }
-                const float O = (((m & 1) ? t0 : 0.f) + ((m & 2) ? t1 : 0.f) + ((m & 4) ? t2 : 0.f) + ((m & 8) ? t3 : 0.f)) * 0.25f;
-                const float w = Te * O * al;
-                C0 += w * rgb[0]; C1 += w * rgb[1]; C2 += w * rgb[2];
-                const float kk = 1.f - al;
-                if (m & 1) t0 *= kk;
-                if (m & 2) t1 *= kk;
-                if (m & 4) t2 *= kk;
-                if (m & 8) t3 *= kk;
-                if (Te * ((t0 + t1) + (t2 + t3)) * 0.25f < bp.t_eps) done = true;
             }
         }
+        __syncwarp();
     }
     if (open) T = Te * ((t0 + t1) + (t2 + t3)) * 0.25f;
     if (COUNT) {

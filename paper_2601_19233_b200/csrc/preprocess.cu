@@ -81,8 +81,11 @@ __device__ __forceinline__ void sh_eval(const float *__restrict__ sh, int deg, f
             r += b[i] * c[3 * i]; g += b[i] * c[3 * i + 1]; bl += b[i] * c[3 * i + 2];
         }
     } else {
-        for (int i = 0; i < k; i++) {
-            r += b[i] * __ldg(sh + 3 * i); g += b[i] * __ldg(sh + 3 * i + 1); bl += b[i] * __ldg(sh + 3 * i + 2);
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            if (i < k) {
+                r += b[i] * __ldg(sh + 3 * i); g += b[i] * __ldg(sh + 3 * i + 1); bl += b[i] * __ldg(sh + 3 * i + 2);
+            }
         }
     }
     out[0] = fmaxf(r + 0.5f, 0.f);
@@ -98,16 +101,20 @@ __global__ void __launch_bounds__(256) k_preprocess_gaussians(GaussInput gin, in
     if (g < gin.N) {
         const int64_t p = F + g;
         uint32_t touched = 0;
+        // all per-Gaussian inputs except SH are loaded up front (one round trip)
+        const float mx = __ldg(gin.means + 3 * g), my = __ldg(gin.means + 3 * g + 1), mz = __ldg(gin.means + 3 * g + 2);
+        const float qw = __ldg(gin.quats + 4 * g), qx = __ldg(gin.quats + 4 * g + 1), qy = __ldg(gin.quats + 4 * g + 2),
+                    qz = __ldg(gin.quats + 4 * g + 3);
+        const float s0 = __ldg(gin.scales + 3 * g), s1 = __ldg(gin.scales + 3 * g + 1), s2 = __ldg(gin.scales + 3 * g + 2);
+        const float o = __ldg(gin.opac + g);
         do {
-            const float mx = __ldg(gin.means + 3 * g), my = __ldg(gin.means + 3 * g + 1), mz = __ldg(gin.means + 3 * g + 2);
             float pv[3];
             view_point(cam, mx, my, mz, pv);
             if (!(pv[2] > cam.near_z) || pv[2] > cam.far_z) break;
             const float xz = dv(pv[0], pv[2]), yz = dv(pv[1], pv[2]);          // N2
             const float u = fma_(cam.fx, xz, cam.cx), v = fma_(cam.fy, yz, cam.cy);
             // N3
-            const float4 q4 = __ldg(reinterpret_cast<const float4 *>(gin.quats) + g);
-            float w = q4.x, x = q4.y, y = q4.z, z = q4.w;
+            float w = qw, x = qx, y = qy, z = qz;
             const float n2 = fma_(w, w, fma_(x, x, fma_(y, y, mul(z, z))));
             const float k = dv(1.0f, __fsqrt_rn(n2));
             w = mul(w, k); x = mul(x, k); y = mul(y, k); z = mul(z, k);
@@ -117,7 +124,6 @@ __global__ void __launch_bounds__(256) k_preprocess_gaussians(GaussInput gin, in
             r[0] = sub(1.0f, mul(2.0f, add(qyy, qzz))); r[1] = mul(2.0f, sub(qxy, qwz)); r[2] = mul(2.0f, add(qxz, qwy));
             r[3] = mul(2.0f, add(qxy, qwz)); r[4] = sub(1.0f, mul(2.0f, add(qxx, qzz))); r[5] = mul(2.0f, sub(qyz, qwx));
             r[6] = mul(2.0f, sub(qxz, qwy)); r[7] = mul(2.0f, add(qyz, qwx)); r[8] = sub(1.0f, mul(2.0f, add(qxx, qyy)));
-            const float s0 = __ldg(gin.scales + 3 * g), s1 = __ldg(gin.scales + 3 * g + 1), s2 = __ldg(gin.scales + 3 * g + 2);
             float m[9];
 #pragma unroll
             for (int a = 0; a < 3; a++) {
@@ -162,7 +168,6 @@ __global__ void __launch_bounds__(256) k_preprocess_gaussians(GaussInput gin, in
             const float ka = mul(cc_, inv), kb = mul(-cb_, inv), kc = mul(ca_, inv);
             if (!(ka > 0.0f && fma_(ka, kc, -mul(kb, kb)) > 0.0f)) break;
             // N5
-            const float o = __ldg(gin.opac + g);
             if (!(255.0 * (double)o >= 1.0)) break;
             const float qmax = (float)(2.0 * log(255.0 * (double)o));
             const float ex = fma_(__fsqrt_rn(mul(qmax, ca_)), 1.0009765625f, 0.00390625f);
