@@ -44,7 +44,10 @@ namespace unimgs {
 constexpr unsigned kFlagAgg = 1, kFlagInc = 2;
 constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
 constexpr int kSortThreads = 256, kSortItems = UNIMGS_SORT_ITEMS, kSortTile = kSortThreads * kSortItems;
-constexpr int kLookWin = 4;  // predecessors inspected per look-back round trip
+#ifndef UNIMGS_LOOKWIN
+#define UNIMGS_LOOKWIN 16
+#endif
+constexpr int kLookWin = UNIMGS_LOOKWIN;  // predecessors inspected per look-back round trip
 
 // scan/pass slots (select the dynamic tile counter and the epoch tag)
 enum { SLOT_COMPACT = 0, SLOT_DUP = 1, SLOT_PASS0 = 2 };
@@ -162,7 +165,7 @@ template <int ITEMS>
 __device__ __forceinline__ void scan_lookback_striped(const unsigned (&val)[ITEMS], unsigned (&excl)[ITEMS],
                                                       unsigned tile, unsigned long long *lb, unsigned tag,
                                                       unsigned *s_w, unsigned &total) {
-    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lane = threadIdx.x & 31;
     unsigned carry = 0;
 #pragma unroll
     for (int i = 0; i < ITEMS; i++) {
@@ -393,7 +396,16 @@ __global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t *__re
 // across it); then a coalesced-by-digit scatter to global memory.
 // ----------------------------------------------------------------------------
 template <typename KT>
-__global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(const KT *__restrict__ kin,
+#ifndef UNIMGS_RANK_MATCH
+#define UNIMGS_RANK_MATCH 0
+#endif
+#ifndef UNIMGS_RANK_ATOMS
+#define UNIMGS_RANK_ATOMS 0
+#endif
+#ifndef UNIMGS_SORT_MINB
+#define UNIMGS_SORT_MINB 2
+#endif
+__global__ void __launch_bounds__(kSortThreads, UNIMGS_SORT_MINB) k_onesweep(const KT *__restrict__ kin,
                                                               const uint32_t *__restrict__ vin, KT *__restrict__ kout,
                                                               uint32_t *__restrict__ vout, const unsigned *n_ptr,
                                                               int shift, int bits, const unsigned *hist, int slot,
@@ -450,14 +462,36 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(const KT *__restri
         }
 #pragma unroll
         for (int i = 0; i < kSortItems; i++) {
+            // stable warp multisplit: the lanes holding the same digit
             const bool valid = wbase + 32u * i < n;
-            const unsigned d = valid ? (unsigned)((key[i] >> shift) & mask) : 256u;
-            const unsigned peers = __match_any_sync(0xffffffffu, d);
-            const unsigned before = d < 256u ? wh[d] : 0u;
+            const unsigned d = valid ? (unsigned)((key[i] >> shift) & mask) : 0u;
+#if UNIMGS_RANK_MATCH
+            const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 256u) & __ballot_sync(0xffffffffu, valid);
+#else
+            // all `bits` ballots first (independent), then combine
+            unsigned bb[8];
+#pragma unroll
+            for (int bt = 0; bt < 8; bt++)
+                if (bt < bits) bb[bt] = __ballot_sync(0xffffffffu, (d >> bt) & 1u);
+            unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+            for (int bt = 0; bt < 8; bt++)
+                if (bt < bits) peers &= ((d >> bt) & 1u) ? bb[bt] : ~bb[bt];
+#endif
+#if UNIMGS_RANK_ATOMS
+            // the group's leader reserves its slots with one shared atomic; in-order per warp,
+            // so earlier items of the same digit are counted first (stable)
+            const int leader = __ffs(peers) - 1;
+            unsigned before = 0;
+            if (valid && lane == (unsigned)leader) before = atomicAdd(&wh[d], (unsigned)__popc(peers));
+            before = __shfl_sync(0xffffffffu, before, valid ? leader : (int)lane);
+#else
+            const unsigned before = valid ? wh[d] : 0u;
+            __syncwarp();
+            if (valid && (peers & lt) == 0) wh[d] = before + __popc(peers);
+            __syncwarp();
+#endif
             rank[i] = before + __popc(peers & lt);
-            __syncwarp();
-            if (d < 256u && (peers & lt) == 0) wh[d] = before + __popc(peers);
-            __syncwarp();
         }
         __syncthreads();
         // per digit: exclusive over warps, block count, publish the aggregate

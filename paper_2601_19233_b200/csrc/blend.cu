@@ -24,6 +24,10 @@
 
 namespace unimgs {
 
+#ifndef UNIMGS_BLEND_PIX
+#define UNIMGS_BLEND_PIX 1
+#endif
+
 struct TexView {
     const uchar4 *tex;
     int w, h;
@@ -111,57 +115,118 @@ __device__ __forceinline__ void tri_colour(const TriRecord &r, const long long E
 //   (10 roundings, cancellation factor <= 2(cond + 1)) errs by < 1.3e-3 q, so a
 //   pixel outside that ellipse cannot satisfy the N6 test q <= q_max.  Other
 //   conics (needles, NaN) are never skipped.
-__device__ __forceinline__ bool gauss_touches(const float4 &a, const float4 &b, float rx0, float ry0) {
+__device__ __forceinline__ bool gauss_touches(const float4 &a, const float4 &b, float rx0, float ry0, float ry1) {
     const float ca = b.x, cb = b.y, cc = b.z;
     const float det = ca * cc - cb * cb, sum = ca + cc;
     if (!(det > 0.f && sum * sum <= 1000.f * det)) return true;
     const float ex = sqrtf(a.z * cc / det) * 1.01f + 0.01f;
     const float ey = sqrtf(a.z * ca / det) * 1.01f + 0.01f;
     if (!(ex < 1e30f && ey < 1e30f)) return true;
-    return a.x + ex >= rx0 && a.x - ex <= rx0 + 7.f && a.y + ey >= ry0 && a.y - ey <= ry0 + 3.f;
+    return a.x + ex >= rx0 && a.x - ex <= rx0 + 7.f && a.y + ey >= ry0 && a.y - ey <= ry1;
 }
 
-__device__ __forceinline__ bool tri_touches(const float4 &a, const float4 &b, int Rx0, int Ry0) {
+__device__ __forceinline__ bool tri_touches(const float4 &a, const float4 &b, int Rx0, int Ry0, int Ry1) {
     const int X0 = __float_as_int(a.x), Y0 = __float_as_int(a.y), X1 = __float_as_int(a.z), Y1 = __float_as_int(a.w);
     const int X2 = __float_as_int(b.x), Y2 = __float_as_int(b.y);
     const int mnx = min(X0, min(X1, X2)), mxx = max(X0, max(X1, X2));
     const int mny = min(Y0, min(Y1, Y2)), mxy = max(Y0, max(Y1, Y2));
-    return mxx >= Rx0 && mnx <= Rx0 + 256 * 8 - 1 && mxy >= Ry0 && mny <= Ry0 + 256 * 4 - 1;
+    return mxx >= Rx0 && mnx <= Rx0 + 256 * 8 - 1 && mxy >= Ry0 && mny <= Ry1;
 }
 
-// One CTA per 16x16 tile, 8 independent warps, one pixel per lane.  Each warp
-// walks the whole tile list in chunks of 32 (lane l holds entry 32c + l; ids are
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Per-pixel blend state (registers).
+struct Px {
+    float C0, C1, C2, T, Te, t0, t1, t2, t3;
+    bool open, done;
+};
+
+// One triangle fragment candidate at pixel (x, y): coverage, then Eq.7-9.
+template <bool COUNT>
+__device__ __forceinline__ void tri_pixel(Px &s, const TriRecord &r, int x, int y, const TexView &tv, float t_eps,
+                                          unsigned long long &w_tt, unsigned long long &w_tf) {
+    const int4 q0 = r.q0, q1 = r.q1;
+    const int X[3] = {q0.x, q0.z, q1.x}, Y[3] = {q0.y, q0.w, q1.y};
+    long long Ec[3];
+    if (COUNT) w_tt++;
+    const unsigned m = coverage(X, Y, x, y, Ec);
+    if (!m) return;
+    if (COUNT) w_tf++;
+    float rgb[3];
+    tri_colour(r, Ec, tv, rgb);
+    const float al = __int_as_float(q1.w);
+    if (!s.open) {
+        s.open = true;
+        s.Te = s.T;
+        s.t0 = s.t1 = s.t2 = s.t3 = 1.f;
+    }
+    const float O = (((m & 1) ? s.t0 : 0.f) + ((m & 2) ? s.t1 : 0.f) + ((m & 4) ? s.t2 : 0.f) + ((m & 8) ? s.t3 : 0.f)) * 0.25f;
+    const float w = s.Te * O * al;
+    s.C0 += w * rgb[0]; s.C1 += w * rgb[1]; s.C2 += w * rgb[2];
+    const float kk = 1.f - al;
+    if (m & 1) s.t0 *= kk;
+    if (m & 2) s.t1 *= kk;
+    if (m & 4) s.t2 *= kk;
+    if (m & 8) s.t3 *= kk;
+    if (s.Te * ((s.t0 + s.t1) + (s.t2 + s.t3)) * 0.25f < t_eps) s.done = true;
+}
+
+// One CTA per 16x16 tile, independent warps, PIX pixels per lane (vertically
+// 4 rows apart).  Warp w owns an 8 x (4 PIX) sub-tile.  Each warp walks the
+// whole tile list in chunks of 32 (lane l holds entry 32c + l; ids are
 // prefetched two chunks ahead and records one chunk ahead), keeps the entries
 // that touch its sub-tile (ballot), packs them into its own shared buffer and
 // blends them in list order with broadcast reads.  No block-wide barrier: a
-// warp stops as soon as all of its pixels have terminated.
-template <bool COUNT>
-__global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2 *__restrict__ ranges,
-                                                            const uint32_t *__restrict__ vals,
-                                                            const GaussRecord *__restrict__ grec,
-                                                            const TriRecord *__restrict__ trec, TexView tv,
-                                                            unsigned F, int W, int H, int tiles_x, BlendParams bp,
-                                                            float4 *__restrict__ out, DevState *st) {
+// warp stops as soon as all of its pixels have terminated.  A packed triangle
+// entry carries q_max = -1, so the Gaussian membership test rejects it for
+// free and only the (rare) miss path checks for triangles.
+#ifndef UNIMGS_BLEND_MINB
+#define UNIMGS_BLEND_MINB (3 * PIX)
+#endif
+template <bool COUNT, int PIX>
+__global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blend(const uint2 *__restrict__ ranges,
+                                                                     const uint32_t *__restrict__ vals,
+                                                                     const GaussRecord *__restrict__ grec,
+                                                                     const TriRecord *__restrict__ trec, TexView tv,
+                                                                     unsigned F, int W, int H, int tiles_x,
+                                                                     BlendParams bp, float4 *__restrict__ out,
+                                                                     DevState *st) {
     if (st->overflow) return;
+    constexpr int NW = kBlendThreads / PIX / 32;  // warps per tile
     unsigned long long w_gt = 0, w_gf = 0, w_tt = 0, w_tf = 0;  // COUNT only
-    __shared__ float4 s_buf[kBlendThreads / 32][32][3];  // per-warp packed entries: a, (ca, 2cb, cc, id), c
+    __shared__ float4 s_buf[NW][32][3];  // per-warp packed entries: a (u, v, q_max, o), (ca, 2cb, cc, id), c
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int sx0 = tx * kTile + (warp & 1) * 8, sy0 = ty * kTile + (warp >> 1) * 4;
-    const int x = sx0 + (lane & 7), y = sy0 + (lane >> 3);
-    const bool inside = x < W && y < H;
-    const float px = (float)x + 0.5f, py = (float)y + 0.5f;
-    const float rx0 = (float)sx0 + 0.5f, ry0 = (float)sy0 + 0.5f;
-    const int Rx0 = 256 * sx0, Ry0 = 256 * sy0;
+    const int sx0 = tx * kTile + (warp & 1) * 8, sy0 = ty * kTile + (warp >> 1) * 4 * PIX;
+    const int x = sx0 + (lane & 7), y0 = sy0 + (lane >> 3);
+    const float px = (float)x + 0.5f;
+    const float rx0 = (float)sx0 + 0.5f, ry0 = (float)sy0 + 0.5f, ry1 = ry0 + (float)(4 * PIX - 1);
+    const int Rx0 = 256 * sx0, Ry0 = 256 * sy0, Ry1 = 256 * (sy0 + 4 * PIX) - 1;
     const uint2 rg = ranges[tile];
     const unsigned lt = (1u << lane) - 1u;
     float4(*buf)[3] = s_buf[warp];
 
-    float C0 = 0.f, C1 = 0.f, C2 = 0.f, T = 1.f, Te = 1.f;
-    float t0 = 1.f, t1 = 1.f, t2 = 1.f, t3 = 1.f;
-    bool open = false, done = !inside;
+    Px s[PIX];
+#pragma unroll
+    for (int p = 0; p < PIX; p++) {
+        s[p].C0 = s[p].C1 = s[p].C2 = 0.f;
+        s[p].T = s[p].Te = 1.f;
+        s[p].t0 = s[p].t1 = s[p].t2 = s[p].t3 = 1.f;
+        s[p].open = false;
+        s[p].done = !(x < W && y0 + 4 * p < H);
+    }
+    auto all_done = [&]() {
+        bool d = true;
+#pragma unroll
+        for (int p = 0; p < PIX; p++) d = d && s[p].done;
+        return d;
+    };
 
     // ids two chunks ahead, records one chunk ahead
     unsigned id1 = rg.x + lane < rg.y ? __ldg(vals + rg.x + lane) : 0xFFFFFFFFu;
@@ -180,80 +245,72 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2 *__restr
         }
     };
     fetch_rec(id1);
+    const float kexp = -0.72134752044448170f;  // -log2(e) / 2
 
     for (unsigned base = rg.x; base < rg.y; base += 32) {
-        if (__all_sync(0xffffffffu, done)) break;
+        if (__all_sync(0xffffffffu, all_done())) break;
         const unsigned id = id1;
         const float4 a = na, b = nb, c = nc;
         id1 = id2;
         id2 = base + 64 + lane < rg.y ? __ldg(vals + base + 64 + lane) : 0xFFFFFFFFu;
         fetch_rec(id1);
         bool rel = false;
-        if (id != 0xFFFFFFFFu) rel = id >= F ? gauss_touches(a, b, rx0, ry0) : tri_touches(a, b, Rx0, Ry0);
+        if (id != 0xFFFFFFFFu)
+            rel = id >= F ? gauss_touches(a, b, rx0, ry0, ry1) : tri_touches(a, b, Rx0, Ry0, Ry1);
         const unsigned bal = __ballot_sync(0xffffffffu, rel);
         if (rel) {
             const unsigned slot = __popc(bal & lt);
-            buf[slot][0] = a;
-            buf[slot][1] = make_float4(b.x, b.y + b.y, b.z, __uint_as_float(id));
-            buf[slot][2] = c;
+            if (id >= F) {
+                buf[slot][0] = a;
+                buf[slot][1] = make_float4(b.x, b.y + b.y, b.z, __uint_as_float(id));
+                buf[slot][2] = c;
+            } else {
+                buf[slot][0] = make_float4(0.f, 0.f, -1.f, 0.f);
+                buf[slot][1] = make_float4(0.f, 0.f, 0.f, __uint_as_float(id));
+            }
         }
         __syncwarp();
         const unsigned cnt = __popc(bal);
         for (unsigned k = 0; k < cnt; k++) {
+            const float4 ea = buf[k][0];
             const float4 eb = buf[k][1];
-            const unsigned eid = __float_as_uint(eb.w);
-            if (eid >= F) {
-                if (COUNT && !done) w_gt++;
-                const float4 ea = buf[k][0];
-                const float dx = __fsub_rn(px, ea.x), dy = __fsub_rn(py, ea.y);
-                const float q = __fmaf_rn(eb.x, __fmul_rn(dx, dx), __fmaf_rn(eb.z, __fmul_rn(dy, dy), __fmul_rn(eb.y, __fmul_rn(dx, dy))));
-                if (q <= ea.z && !done) {
+            const float dx = __fsub_rn(px, ea.x);
+            const float dxx = __fmul_rn(dx, dx);
+            bool hit[PIX], any = false;
+            float q[PIX];
+#pragma unroll
+            for (int p = 0; p < PIX; p++) {
+                const float dy = __fsub_rn((float)(y0 + 4 * p) + 0.5f, ea.y);
+                q[p] = __fmaf_rn(eb.x, dxx, __fmaf_rn(eb.z, __fmul_rn(dy, dy), __fmul_rn(eb.y, __fmul_rn(dx, dy))));
+                hit[p] = q[p] <= ea.z && !s[p].done;
+                if (COUNT && ea.z >= 0.f && !s[p].done) w_gt++;
+                any = any || hit[p];
+            }
+            if (any) {
+                const float4 ec = buf[k][2];
+#pragma unroll
+                for (int p = 0; p < PIX; p++) {
+                    if (!hit[p]) continue;
                     if (COUNT) w_gf++;
-                    const float al = fminf(bp.alpha_max, ea.w * __expf(-0.5f * q));
-                    if (open) {
-                        T = Te * ((t0 + t1) + (t2 + t3)) * 0.25f;
-                        open = false;
+                    const float al = fminf(bp.alpha_max, ea.w * ex2_ftz(q[p] * kexp));
+                    if (s[p].open) {
+                        s[p].T = s[p].Te * ((s[p].t0 + s[p].t1) + (s[p].t2 + s[p].t3)) * 0.25f;
+                        s[p].open = false;
                     }
-                    const float4 ec = buf[k][2];
-                    const float w = T * al;
-                    C0 += w * ec.x; C1 += w * ec.y; C2 += w * ec.z;
-                    T -= w;
-                    if (T < bp.t_eps) done = true;
+                    const float w = s[p].T * al;
+                    s[p].C0 += w * ec.x; s[p].C1 += w * ec.y; s[p].C2 += w * ec.z;
+                    s[p].T -= w;
+                    if (s[p].T < bp.t_eps) s[p].done = true;
                 }
-            } else if (!done) {
-                const TriRecord &r = trec[eid];
-                const int4 q0 = r.q0, q1 = r.q1;
-                const int X[3] = {q0.x, q0.z, q1.x}, Y[3] = {q0.y, q0.w, q1.y};
-                long long Ec[3];
-                if (COUNT) w_tt++;
-                const unsigned m = coverage(X, Y, x, y, Ec);
-                if (m) {
-                    if (COUNT) w_tf++;
-                    TriRecord rr;
-                    rr.q0 = q0; rr.q1 = q1; rr.q2 = r.q2; rr.q3 = r.q3; rr.q4 = r.q4; rr.q5 = r.q5;
-                    float rgb[3];
-                    tri_colour(rr, Ec, tv, rgb);
-                    const float al = __int_as_float(q1.w);
-                    if (!open) {
-                        open = true;
-                        Te = T;
-                        t0 = t1 = t2 = t3 = 1.f;
-                    }
-                    const float O = (((m & 1) ? t0 : 0.f) + ((m & 2) ? t1 : 0.f) + ((m & 4) ? t2 : 0.f) + ((m & 8) ? t3 : 0.f)) * 0.25f;
-                    const float w = Te * O * al;
-                    C0 += w * rgb[0]; C1 += w * rgb[1]; C2 += w * rgb[2];
-                    const float kk = 1.f - al;
-                    if (m & 1) t0 *= kk;
-                    if (m & 2) t1 *= kk;
-                    if (m & 4) t2 *= kk;
-                    if (m & 8) t3 *= kk;
-                    if (Te * ((t0 + t1) + (t2 + t3)) * 0.25f < bp.t_eps) done = true;
-                }
+            } else if (ea.z < 0.f) {
+                const TriRecord &r = trec[__float_as_uint(eb.w)];
+#pragma unroll
+                for (int p = 0; p < PIX; p++)
+                    if (!s[p].done) tri_pixel<COUNT>(s[p], r, x, y0 + 4 * p, tv, bp.t_eps, w_tt, w_tf);
             }
         }
         __syncwarp();
     }
-    if (open) T = Te * ((t0 + t1) + (t2 + t3)) * 0.25f;
     if (COUNT) {
         unsigned long long v[4] = {w_gt, w_gf, w_tt, w_tf};
 #pragma unroll
@@ -264,23 +321,32 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2 *__restr
             if (lane == 0 && xs) atomicAdd(&st->work[k], xs);
         }
     }
-    if (inside) {
-        const float s = T * bp.bg_alpha;
-        out[(size_t)y * W + x] = make_float4(C0 + s * bp.bg[0], C1 + s * bp.bg[1], C2 + s * bp.bg[2], T);
+#pragma unroll
+    for (int p = 0; p < PIX; p++) {
+        const int y = y0 + 4 * p;
+        if (x < W && y < H) {
+            float T = s[p].T;
+            if (s[p].open) T = s[p].Te * ((s[p].t0 + s[p].t1) + (s[p].t2 + s[p].t3)) * 0.25f;
+            const float sb = T * bp.bg_alpha;
+            out[(size_t)y * W + x] = make_float4(s[p].C0 + sb * bp.bg[0], s[p].C1 + sb * bp.bg[1], s[p].C2 + sb * bp.bg[2], T);
+        }
     }
 }
 
 int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, const CamParams &cam,
                  const BlendParams &bp, float *out, cudaStream_t s, bool count_work) {
     (void)g;
+    constexpr int PIX = UNIMGS_BLEND_PIX;
     const int tiles = cam.tiles_x * cam.tiles_y;
     TexView tv{reinterpret_cast<const uchar4 *>(m.tex), m.tw, m.th};
     if (count_work)
-        k_blend<true><<<tiles, kBlendThreads, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv, (unsigned)m.F, cam.W,
-                                                      cam.H, cam.tiles_x, bp, reinterpret_cast<float4 *>(out), b.st);
+        k_blend<true, PIX><<<tiles, kBlendThreads / PIX, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv,
+                                                                 (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
+                                                                 reinterpret_cast<float4 *>(out), b.st);
     else
-        k_blend<false><<<tiles, kBlendThreads, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv, (unsigned)m.F, cam.W,
-                                                       cam.H, cam.tiles_x, bp, reinterpret_cast<float4 *>(out), b.st);
+        k_blend<false, PIX><<<tiles, kBlendThreads / PIX, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv,
+                                                                  (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
+                                                                  reinterpret_cast<float4 *>(out), b.st);
     return 1;
 }
 

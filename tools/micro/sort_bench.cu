@@ -1,0 +1,67 @@
+// Standalone timing of the onesweep passes (includes binning.cu): random u16 tile keys
+// (K pairs, 13-bit) and u32 depth keys; checks the result is sorted and stable.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <numeric>
+#include <vector>
+#include "../../paper_2601_19233_b200/csrc/binning.cu"
+using namespace unimgs;
+
+template <typename KT>
+static float run(int n, int bits, int reps, bool check) {
+    std::vector<KT> hk(n);
+    std::vector<uint32_t> hv(n);
+    srand(1);
+    for (int i = 0; i < n; i++) { hk[i] = (KT)(rand() & ((1u << bits) - 1)); hv[i] = i; }
+    KT *k[2]; uint32_t *v[2];
+    for (int i = 0; i < 2; i++) { cudaMalloc(&k[i], n * sizeof(KT)); cudaMalloc(&v[i], n * 4); }
+    unsigned long long *lb; cudaMalloc(&lb, (size_t)8 * 256 * (n / 1024 + 16));
+    cudaMemset(lb, 0, (size_t)8 * 256 * (n / 1024 + 16));
+    DevState *st; cudaMalloc(&st, sizeof(DevState));
+    Buffers b{}; b.lookback = lb; b.st = st;
+    std::vector<unsigned> hist(8 * 256, 0);
+    for (int i = 0; i < n; i++) for (int p = 0, sh = 0; sh < bits; p++, sh += 8) hist[p * 256 + ((hk[i] >> sh) & 255)]++;
+    DevState hs{}; hs.n_vis = n; hs.K = n;
+    memcpy(hs.hist, hist.data(), sizeof(hs.hist));
+    int dev; cudaGetDevice(&dev); int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    set_attrs();
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float best = 1e9;
+    for (int r = 0; r < reps; r++) {
+        hs.frame_epoch = r + 1;
+        cudaMemcpy(st, &hs, sizeof hs, cudaMemcpyHostToDevice);
+        cudaMemcpy(k[0], hk.data(), n * sizeof(KT), cudaMemcpyHostToDevice);
+        cudaMemcpy(v[0], hv.data(), n * 4, cudaMemcpyHostToDevice);
+        cudaEventRecord(e0);
+        int c = 0, slot = 2;
+        for (int p = 0, sh = 0; sh < bits; p++, sh += 8, slot++) {
+            onesweep_pass<KT>(b, k[c], v[c], k[c ^ 1], v[c ^ 1], &st->K, sh, std::min(8, bits - sh), p, slot,
+                              sort_grid(n, sms, 2), 0);
+            c ^= 1;
+        }
+        cudaEventRecord(e1); cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        best = std::min(best, ms);
+        if (check && r == reps - 1) {
+            std::vector<KT> ok(n); std::vector<uint32_t> ov(n);
+            cudaMemcpy(ok.data(), k[c], n * sizeof(KT), cudaMemcpyDeviceToHost);
+            cudaMemcpy(ov.data(), v[c], n * 4, cudaMemcpyDeviceToHost);
+            std::vector<uint32_t> idx(n); std::iota(idx.begin(), idx.end(), 0);
+            std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t bb) { return hk[a] < hk[bb]; });
+            bool good = true;
+            for (int i = 0; i < n && good; i++) good = ov[i] == idx[i] && ok[i] == hk[idx[i]];
+            printf("  check %s\n", good ? "OK" : "FAILED");
+        }
+    }
+    printf("%s n=%d bits=%d: %.1f us (%.2f GB/s per pass moved)\n", sizeof(KT) == 2 ? "u16" : "u32", n, bits,
+           best * 1e3, (double)n * (2 * sizeof(KT) + 8) * ((bits + 7) / 8) / (best * 1e-3) / 1e9);
+    return best;
+}
+
+int main() {
+    run<uint16_t>(7480746, 13, 5, true);
+    run<uint32_t>(1551224, 32, 5, true);
+    run<uint32_t>(1551224, 16, 5, false);
+    return 0;
+}

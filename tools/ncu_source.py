@@ -15,6 +15,11 @@ def main():
     cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}"]
     out = subprocess.check_output(cmd, text=True, stderr=subprocess.DEVNULL)
     lines = out.splitlines()
+    # several launches may match: keep the section of the --nth one (default 0)
+    nth = int(sys.argv[sys.argv.index("--nth") + 1]) if "--nth" in sys.argv else 0
+    starts = [i for i, l in enumerate(lines) if l.startswith('"Kernel Name"')] + [len(lines)]
+    lines = lines[starts[nth]:starts[nth + 1]]
+    print(lines[0][:160])
     rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
     h = rows[0]
     si = h.index("Warp Stall Sampling (All Samples)")
