@@ -185,7 +185,8 @@ UNIMGS_API int unimgs_get_bins(unimgs_ctx *c, uint64_t *keys, uint32_t *vals, ui
 
 /* Debug copy of the per-primitive records into caller device buffers (any
  * may be NULL):
- *   grec   [N][12] float: u, v, q_max, o, conic a, b, c, depth, r, g, b, 0
+ *   grec   [N][12] float: u, v, q_max, o, conic a, b, c, cull half-extent y,
+ *          r, g, b, cull half-extent x (-1 = never culled; depth is in depth_keys)
  *   trec   [F][24] 32-bit words: X0 Y0 X1 Y1 X2 Y2 (int32, 1/256 px, after
  *          the orientation swap), shading kind, alpha bits, z0 z1 z2 depth,
  *          then 9 attribute floats, then padding

@@ -111,17 +111,15 @@ __device__ __forceinline__ void tri_colour(const TriRecord &r, const long long E
 //   triangle: its snapped integer bbox misses the sub-tile's 1/256-px extent;
 //   Gaussian: the sub-tile's pixel centres lie outside the bbox of the exact
 //   ellipse {d : Q(d) <= q_max (1 + 0.02)} of the fp32 conic Q, padded by
-//   1% + 0.01 px.  Only for cond(Q) <= ~1000, where the fp32 evaluation of q
-//   (10 roundings, cancellation factor <= 2(cond + 1)) errs by < 1.3e-3 q, so a
-//   pixel outside that ellipse cannot satisfy the N6 test q <= q_max.  Other
-//   conics (needles, NaN) are never skipped.
-__device__ __forceinline__ bool gauss_touches(const float4 &a, const float4 &b, float rx0, float ry0, float ry1) {
-    const float ca = b.x, cb = b.y, cc = b.z;
-    const float det = ca * cc - cb * cb, sum = ca + cc;
-    if (!(det > 0.f && sum * sum <= 1000.f * det)) return true;
-    const float ex = sqrtf(a.z * cc / det) * 1.01f + 0.01f;
-    const float ey = sqrtf(a.z * ca / det) * 1.01f + 0.01f;
-    if (!(ex < 1e30f && ey < 1e30f)) return true;
+//   1% + 0.01 px (half-extents computed once per Gaussian in B1).  Only for
+//   cond(Q) <= ~1000, where the fp32 evaluation of q (10 roundings,
+//   cancellation factor <= 2(cond + 1)) errs by < 1.3e-3 q, so a pixel outside
+//   that ellipse cannot satisfy the N6 test q <= q_max.  Other conics
+//   (needles, NaN) are never skipped.
+__device__ __forceinline__ bool gauss_touches(const float4 &a, const float4 &b, const float4 &c, float rx0, float ry0,
+                                              float ry1) {
+    const float ex = c.w, ey = b.w;  // precomputed in B1; -1 = never cull
+    if (!(ex >= 0.f)) return true;
     return a.x + ex >= rx0 && a.x - ex <= rx0 + 7.f && a.y + ey >= ry0 && a.y - ey <= ry1;
 }
 
@@ -256,8 +254,9 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
         fetch_rec(id1);
         bool rel = false;
         if (id != 0xFFFFFFFFu)
-            rel = id >= F ? gauss_touches(a, b, rx0, ry0, ry1) : tri_touches(a, b, Rx0, Ry0, Ry1);
+            rel = id >= F ? gauss_touches(a, b, c, rx0, ry0, ry1) : tri_touches(a, b, Rx0, Ry0, Ry1);
         const unsigned bal = __ballot_sync(0xffffffffu, rel);
+        const bool has_tri = __any_sync(0xffffffffu, rel && id < F);
         if (rel) {
             const unsigned slot = __popc(bal & lt);
             if (id >= F) {
@@ -271,9 +270,8 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
         }
         __syncwarp();
         const unsigned cnt = __popc(bal);
-        for (unsigned k = 0; k < cnt; k++) {
-            const float4 ea = buf[k][0];
-            const float4 eb = buf[k][1];
+        // Gaussian fragment test + blend (Eq.1-2) of packed entry k for each pixel
+        auto gauss = [&](const float4 &ea, const float4 &eb, unsigned k) {
             const float dx = __fsub_rn(px, ea.x);
             const float dxx = __fmul_rn(dx, dx);
             bool hit[PIX], any = false;
@@ -286,27 +284,44 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
                 if (COUNT && ea.z >= 0.f && !s[p].done) w_gt++;
                 any = any || hit[p];
             }
-            if (any) {
-                const float4 ec = buf[k][2];
+            if (!any) return false;
+            const float4 ec = buf[k][2];
 #pragma unroll
-                for (int p = 0; p < PIX; p++) {
-                    if (!hit[p]) continue;
-                    if (COUNT) w_gf++;
-                    const float al = fminf(bp.alpha_max, ea.w * ex2_ftz(q[p] * kexp));
-                    if (s[p].open) {
-                        s[p].T = s[p].Te * ((s[p].t0 + s[p].t1) + (s[p].t2 + s[p].t3)) * 0.25f;
-                        s[p].open = false;
-                    }
-                    const float w = s[p].T * al;
-                    s[p].C0 += w * ec.x; s[p].C1 += w * ec.y; s[p].C2 += w * ec.z;
-                    s[p].T -= w;
-                    if (s[p].T < bp.t_eps) s[p].done = true;
+            for (int p = 0; p < PIX; p++) {
+                if (!hit[p]) continue;
+                if (COUNT) w_gf++;
+                const float al = fminf(bp.alpha_max, ea.w * ex2_ftz(q[p] * kexp));
+                if (s[p].open) {
+                    s[p].T = s[p].Te * ((s[p].t0 + s[p].t1) + (s[p].t2 + s[p].t3)) * 0.25f;
+                    s[p].open = false;
                 }
-            } else if (ea.z < 0.f) {
-                const TriRecord &r = trec[__float_as_uint(eb.w)];
+                const float w = s[p].T * al;
+                s[p].C0 += w * ec.x; s[p].C1 += w * ec.y; s[p].C2 += w * ec.z;
+                s[p].T -= w;
+                if (s[p].T < bp.t_eps) s[p].done = true;
+            }
+            return true;
+        };
+        if (!has_tri) {
+            // Gaussian-only chunk: two entries per iteration (independent q chains)
+            unsigned k = 0;
+            for (; k + 2 <= cnt; k += 2) {
+                const float4 ea0 = buf[k][0], eb0 = buf[k][1], ea1 = buf[k + 1][0], eb1 = buf[k + 1][1];
+                gauss(ea0, eb0, k);
+                gauss(ea1, eb1, k + 1);
+            }
+            if (k < cnt) gauss(buf[k][0], buf[k][1], k);
+        } else {
+            for (unsigned k = 0; k < cnt; k++) {
+                const float4 ea = buf[k][0];
+                const float4 eb = buf[k][1];
+                if (gauss(ea, eb, k)) continue;
+                if (ea.z < 0.f) {
+                    const TriRecord &r = trec[__float_as_uint(eb.w)];
 #pragma unroll
-                for (int p = 0; p < PIX; p++)
-                    if (!s[p].done) tri_pixel<COUNT>(s[p], r, x, y0 + 4 * p, tv, bp.t_eps, w_tt, w_tf);
+                    for (int p = 0; p < PIX; p++)
+                        if (!s[p].done) tri_pixel<COUNT>(s[p], r, x, y0 + 4 * p, tv, bp.t_eps, w_tt, w_tf);
+                }
             }
         }
         __syncwarp();

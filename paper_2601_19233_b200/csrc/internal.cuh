@@ -50,7 +50,8 @@ struct TriRecord {
     float4 q2, q3, q4, q5;
 };
 
-// Gaussian record, 48 B: {u, v, q_max, o}, {ca, cb, cc, depth}, {r, g, b, 0}.
+// Gaussian record, 48 B: {u, v, q_max, o}, {ca, cb, cc, cull_ey}, {r, g, b, cull_ex}
+// (cull_e* = half-extents of the blend's exact per-warp culling, -1 = never cull).
 struct GaussRecord {
     float4 a, b, c;
 };

@@ -185,10 +185,21 @@ __global__ void __launch_bounds__(256) k_preprocess_gaussians(GaussInput gin, in
             float rgb[3];
             const int kc3 = (gin.sh_degree + 1) * (gin.sh_degree + 1) * 3;
             sh_eval(gin.sh + g * kc3, gin.sh_degree, dxw * rn, dyw * rn, dzw * rn, rgb);
+            // half-extents of the blend's exact per-warp culling (see blend.cu): the bbox of
+            // {d : Q(d) <= q_max (1 + 0.02)} of the fp32 conic Q, padded; -1 = never cull
+            float cex = -1.f, cey = -1.f;
+            {
+                const float cdet = ka * kc - kb * kb, csum = ka + kc;
+                if (cdet > 0.f && csum * csum <= 1000.f * cdet) {
+                    const float ex2 = sqrtf(qmax * kc / cdet) * 1.01f + 0.01f;
+                    const float ey2 = sqrtf(qmax * ka / cdet) * 1.01f + 0.01f;
+                    if (ex2 < 1e30f && ey2 < 1e30f) { cex = ex2; cey = ey2; }
+                }
+            }
             GaussRecord rec;
             rec.a = make_float4(u, v, qmax, o);
-            rec.b = make_float4(ka, kb, kc, pv[2]);
-            rec.c = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+            rec.b = make_float4(ka, kb, kc, cey);
+            rec.c = make_float4(rgb[0], rgb[1], rgb[2], cex);
             b.grec[g] = rec;
             b.rect[p] = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 16), (uint32_t)x1 | ((uint32_t)y1 << 16));
             b.dkey[p] = __float_as_uint(pv[2]);
