@@ -145,7 +145,12 @@ struct Px {
 
 // One triangle fragment candidate at pixel (x, y): coverage, then Eq.7-9.
 template <bool COUNT>
-__device__ __forceinline__ void tri_pixel(Px &s, const TriRecord &r, int x, int y, const TexView &tv, float t_eps,
+#ifdef UNIMGS_TRI_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void tri_pixel(Px &s, const TriRecord &r, int x, int y, const TexView &tv, float t_eps,
                                           unsigned long long &w_tt, unsigned long long &w_tf) {
     const int4 q0 = r.q0, q1 = r.q1;
     const int X[3] = {q0.x, q0.z, q1.x}, Y[3] = {q0.y, q0.w, q1.y};
@@ -183,7 +188,7 @@ __device__ __forceinline__ void tri_pixel(Px &s, const TriRecord &r, int x, int 
 // entry carries q_max = -1, so the Gaussian membership test rejects it for
 // free and only the (rare) miss path checks for triangles.
 #ifndef UNIMGS_BLEND_MINB
-#define UNIMGS_BLEND_MINB (3 * PIX)
+#define UNIMGS_BLEND_MINB (4 * PIX)
 #endif
 template <bool COUNT, int PIX>
 __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blend(const uint2 *__restrict__ ranges,
