@@ -6,17 +6,17 @@
 // tile << 32 | bits(depth) with ties by id (readings R8, R9, R23).
 //
 // Pipeline (both sort modes produce the identical order):
-//   k_compact        visible primitives in id order (decoupled look-back scan)
-//                    and every digit histogram the radix passes need: depth
-//                    digits per primitive, tile digits of all pairs computed
-//                    per rect row (no per-pair atomics);
-//   k_tile_lo_hist   low tile digit histogram from its difference array.
+//   k_scan_counts + k_compact   visible primitives in id order, reduce-then-
+//                    scan over the per-CTA counts written by B1/B2 (no chains);
+//   k_hist_depth     depth-digit histograms of the compacted keys.
 //   sort_mode 0 (factored, default):
 //     k_onesweep<u32> x4   stable LSD on the 32-bit depth key of the visible
 //                          primitives (id ties stay in id order);
-//     k_duplicate<false>   scan of tiles_touched in depth order fused with the
-//                          emission of (u16 tile, u32 id) pairs, staged through
-//                          shared memory so every store is coalesced;
+//     k_dup_count + k_scan_counts + k_duplicate<false>   tiles_touched scan in
+//                          depth order (reduce-then-scan, sets K and the capacity
+//                          flag) and emission of (u16 tile, u32 id) pairs staged
+//                          through shared memory so every store is coalesced,
+//                          with the tile-digit histograms of the radix passes;
 //     k_onesweep<u16> x2   stable LSD on the tile id: pairs emitted in
 //                          (depth, id) order come out in (tile, depth, id)
 //                          order -- ~4x fewer bytes than sorting K 64-bit keys;
@@ -87,85 +87,161 @@ __device__ __forceinline__ unsigned claim_tile(unsigned *ctr, unsigned *s_tile) 
 }
 
 // ----------------------------------------------------------------------------
-// Block-wide exclusive scan of ITEMS saturating u32 values per thread plus the
-// decoupled look-back across tiles (warp 0 inspects 32 predecessors at once).
-// s_w needs 10 entries.  Returns the inclusive grand total through `total`.
+// Reduce-then-scan (no look-back chains):
+//   B1/B2 write one visible count per CTA of 256 primitives (bcnt);
+//   k_scan_counts scans a count array in place in one CTA;
+//   k_compact writes every visible primitive at its CTA offset + local rank;
+//   k_dup_count / k_scan_counts / k_duplicate do the same for the pairs.
 // ----------------------------------------------------------------------------
-template <int ITEMS>
-__device__ __forceinline__ void scan_lookback(const unsigned (&val)[ITEMS], unsigned (&excl)[ITEMS], unsigned tile,
-                                              unsigned long long *lb, unsigned tag, unsigned *s_w, unsigned &total) {
+// mode 0: total -> st->n_vis; mode 1: total -> needed / overflow / K (cap check)
+__global__ void __launch_bounds__(1024) k_scan_counts(uint32_t *cnt, int64_t n, int mode, int64_t cap, DevState *st) {
+    __shared__ unsigned s_w[32];
+    __shared__ unsigned s_carry;
     const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned tsum = 0;
-#pragma unroll
-    for (int i = 0; i < ITEMS; i++) tsum = sat_add(tsum, val[i]);
-    unsigned x = tsum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= (unsigned)o) x = sat_add(x, y);
-    }
-    const unsigned wexcl = __shfl_up_sync(0xffffffffu, x, 1);
-    const unsigned my_wexcl = lane ? wexcl : 0u;
-    if (lane == 31) s_w[wid] = x;
+    if (threadIdx.x == 0) s_carry = 0;
     __syncthreads();
-    if (wid == 0) {
-        const unsigned nw = blockDim.x >> 5;
-        const unsigned wv = lane < nw ? s_w[lane] : 0u;
-        unsigned wi = wv;
+    for (int64_t c0 = 0; c0 < n; c0 += 4 * 1024) {
+        unsigned v[4], tsum = 0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int64_t i = c0 + 4 * (int64_t)threadIdx.x + j;
+            v[j] = i < n ? cnt[i] : 0u;
+            tsum = sat_add(tsum, v[j]);
+        }
+        unsigned x = tsum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= (unsigned)o) wi = sat_add(wi, y);
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (unsigned)o) x = sat_add(x, y);
         }
-        const unsigned agg = __shfl_sync(0xffffffffu, wi, 31);
-        const unsigned wex = __shfl_up_sync(0xffffffffu, wi, 1);
-        unsigned prefix = 0;
-        if (tile == 0) {
-            if (lane == 0) st_relaxed(lb, pack(tag, kFlagInc, agg));
-        } else {
-            if (lane == 0) st_relaxed(lb + tile, pack(tag, kFlagAgg, agg));
-            int j = (int)tile - 1;
-            while (true) {
-                const int idx = j - (int)lane;
-                unsigned flag = kFlagInc, v = 0;
-                if (idx >= 0) {
-                    const unsigned long long e = ld_relaxed(lb + idx);
-                    const unsigned hi = (unsigned)(e >> 32);
-                    flag = ((hi >> 2) == tag) ? (hi & 3u) : 0u;
-                    v = (unsigned)e;
-                }
-                if (__any_sync(0xffffffffu, flag == 0)) continue;
-                const unsigned incm = __ballot_sync(0xffffffffu, flag == kFlagInc);
-                const int first = __ffs(incm) - 1;
-                unsigned c = (first < 0 || (int)lane <= first) ? v : 0u;
+        const unsigned xe = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane == 31) s_w[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            unsigned w = s_w[lane];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) c = sat_add(c, __shfl_xor_sync(0xffffffffu, c, o));
-                prefix = sat_add(prefix, c);
-                if (incm) break;
-                j -= 32;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= (unsigned)o) w = sat_add(w, y);
             }
-            if (lane == 0) st_relaxed(lb + tile, pack(tag, kFlagInc, sat_add(prefix, agg)));
+            s_w[lane] = w;
         }
-        if (lane < nw) s_w[lane] = sat_add(prefix, lane ? wex : 0u);
-        if (lane == 0) s_w[8] = sat_add(prefix, agg);
-    }
-    __syncthreads();
-    unsigned run = sat_add(s_w[wid], my_wexcl);
+        __syncthreads();
+        const unsigned carry = s_carry;
+        unsigned run = sat_add(carry, sat_add(wid ? s_w[wid - 1] : 0u, lane ? xe : 0u));
 #pragma unroll
-    for (int i = 0; i < ITEMS; i++) {
-        excl[i] = run;
-        run = sat_add(run, val[i]);
+        for (int j = 0; j < 4; j++) {
+            const int64_t i = c0 + 4 * (int64_t)threadIdx.x + j;
+            if (i < n) cnt[i] = run;
+            run = sat_add(run, v[j]);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = sat_add(carry, s_w[31]);
+        __syncthreads();
     }
-    total = s_w[8];
+    if (threadIdx.x == 0) {
+        const unsigned total = s_carry;
+        if (mode == 0) {
+            st->n_vis = total;
+        } else {
+            st->needed = total;
+            const bool over = (int64_t)total > cap;
+            st->overflow = over ? 1u : 0u;
+            st->K = over ? 0u : total;
+        }
+    }
 }
 
-// Same scan for a warp-striped arrangement: item i of lane l of warp w is element
-// base + w * 32 * ITEMS + i * 32 + l (coalesced loads); offsets follow index order.
+// One CTA per 256 primitives, in the block order of B2 (triangles) then B1 (Gaussians).
+__global__ void __launch_bounds__(256) k_compact(int64_t F, int64_t N, int nbt, const uint32_t *__restrict__ touched,
+                                                 const uint32_t *__restrict__ dkey, const uint32_t *__restrict__ boff,
+                                                 uint32_t *ok, uint32_t *ov) {
+    __shared__ unsigned s_c[8];
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int blk = blockIdx.x;
+    int64_t p;
+    bool in;
+    if (blk < nbt) {
+        p = (int64_t)blk * 256 + threadIdx.x;
+        in = p < F;
+    } else {
+        const int64_t g = (int64_t)(blk - nbt) * 256 + threadIdx.x;
+        in = g < N;
+        p = F + g;
+    }
+    const bool v = in && touched[p] > 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, v);
+    if (lane == 0) s_c[wid] = __popc(bal);
+    __syncthreads();
+    if (v) {
+        unsigned pos = boff[blk] + __popc(bal & ((1u << lane) - 1u));
+        for (unsigned w = 0; w < wid; w++) pos += s_c[w];
+        ok[pos] = dkey[p];
+        ov[pos] = (uint32_t)p;
+    }
+}
+
+// Pair counts of CTA-sized runs (kScanTile) of the (sorted) visible primitives.
+__global__ void __launch_bounds__(kScanThreads) k_dup_count(const uint32_t *__restrict__ ids,
+                                                            const uint32_t *__restrict__ touched, uint32_t *dcnt,
+                                                            const DevState *st) {
+    __shared__ unsigned s_w[8];
+    const unsigned n = st->n_vis;
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    unsigned sum = 0;
+    if (base < n) {
+#pragma unroll
+        for (int i = 0; i < kScanItems; i++) {
+            const int64_t j = base + (int64_t)i * kScanThreads + threadIdx.x;
+            if (j < n) sum = sat_add(sum, touched[ids[j]]);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum = sat_add(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+    if (lane == 0) s_w[wid] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t = 0;
+        for (int w = 0; w < kScanThreads / 32; w++) t = sat_add(t, s_w[w]);
+        dcnt[blockIdx.x] = t;
+    }
+}
+
+// Depth-digit histograms (4 x 256 bins) of the compacted depth keys, for the
+// four depth passes.  Persistent CTAs, CTA-shared histograms for the three low
+// digits and warp-private ones for the top digit (few distinct exponent bytes:
+// the contended one), one flush per CTA.
+__global__ void __launch_bounds__(256) k_hist_depth(const uint32_t *__restrict__ keys, DevState *st) {
+    __shared__ unsigned s_h[3 * 256];
+    __shared__ unsigned s_top[8][256];
+    for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) s_h[i] = 0;
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&s_top[0][0])[i] = 0;
+    __syncthreads();
+    const unsigned n = st->n_vis, wid = threadIdx.x >> 5;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        atomicAdd(&s_h[k & 255u], 1u);
+        atomicAdd(&s_h[256 + ((k >> 8) & 255u)], 1u);
+        atomicAdd(&s_h[512 + ((k >> 16) & 255u)], 1u);
+        atomicAdd(&s_top[wid][k >> 24], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x)
+        if (s_h[i]) atomicAdd(&st->hist[HIST_DEPTH0 + i / 256][i % 256], s_h[i]);
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        unsigned t = 0;
+        for (int w = 0; w < 8; w++) t += s_top[w][i];
+        if (t) atomicAdd(&st->hist[HIST_DEPTH0 + 3][i], t);
+    }
+}
+
+// Block-wide exclusive scan of warp-striped items (item i of lane l of warp w is
+// element w * 32 * ITEMS + i * 32 + l), saturating u32.
 template <int ITEMS>
-__device__ __forceinline__ void scan_lookback_striped(const unsigned (&val)[ITEMS], unsigned (&excl)[ITEMS],
-                                                      unsigned tile, unsigned long long *lb, unsigned tag,
-                                                      unsigned *s_w, unsigned &total) {
-    const unsigned lane = threadIdx.x & 31;
+__device__ __forceinline__ void block_scan_striped(const unsigned (&val)[ITEMS], unsigned (&excl)[ITEMS],
+                                                   unsigned *s_w) {
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned carry = 0;
 #pragma unroll
     for (int i = 0; i < ITEMS; i++) {
@@ -179,125 +255,12 @@ __device__ __forceinline__ void scan_lookback_striped(const unsigned (&val)[ITEM
         excl[i] = sat_add(carry, lane ? e : 0u);
         carry = sat_add(carry, __shfl_sync(0xffffffffu, x, 31));
     }
-    // reuse the blocked scan for the warp totals: lane 0 contributes its warp's total
-    unsigned wv[1] = {lane == 0 ? carry : 0u}, wx[1];
-    scan_lookback<1>(wv, wx, tile, lb, tag, s_w, total);
-    const unsigned wbase = __shfl_sync(0xffffffffu, wx[0], 0);
-#pragma unroll
-    for (int i = 0; i < ITEMS; i++) excl[i] = sat_add(wbase, excl[i]);
-}
-
-// Tile-digit histograms of a primitive's pairs, per rect row: the low digit
-// (t & 255) of a run of consecutive tile ids is a cyclic range of bins
-// (difference array d_lo[257] + full cycles), the high digit (t >> 8) takes
-// one or two values.  Exact pair counts with O(rows) shared atomics.
-__device__ __forceinline__ void tile_digit_hist(uint2 r, int tiles_x, unsigned *d_lo, unsigned *h_hi,
-                                                unsigned *all_lo) {
-    const unsigned x0 = r.x & 0xFFFF, y0 = r.x >> 16, x1 = r.y & 0xFFFF, y1 = r.y >> 16;
-    for (unsigned ty = y0; ty <= y1; ty++) {
-        const unsigned a = ty * (unsigned)tiles_x + x0, b = ty * (unsigned)tiles_x + x1;
-        const unsigned len = b - a + 1, full = len >> 8, rem = len & 255u;
-        if (full) atomicAdd(all_lo, full);
-        if (rem) {
-            const unsigned lo = a & 255u, e = lo + rem;
-            if (e <= 256u) {
-                atomicAdd(d_lo + lo, 1u);
-                atomicAdd(d_lo + e, 0xFFFFFFFFu);
-            } else {
-                atomicAdd(d_lo + lo, 1u);
-                atomicAdd(d_lo + 256, 0xFFFFFFFFu);
-                atomicAdd(d_lo + 0, 1u);
-                atomicAdd(d_lo + (e - 256u), 0xFFFFFFFFu);
-            }
-        }
-        for (unsigned h = a >> 8; h <= (b >> 8); h++) {
-            const unsigned s0 = max(a, h << 8), s1 = min(b, (h << 8) + 255u);
-            atomicAdd(h_hi + (h & 255u), s1 - s0 + 1);
-        }
-    }
-}
-
-// ----------------------------------------------------------------------------
-// k_compact: visible primitives (touched > 0) in id order -> (depth key, id),
-// warp-striped (coalesced) with a ballot scan.  Histograms for the radix
-// passes: depth digits of the primitive keys (factored) or of the pair keys
-// (FULL: weighted by tiles_touched), and the two tile digits of all pairs.
-// ----------------------------------------------------------------------------
-template <bool FULL>
-__global__ void __launch_bounds__(kScanThreads) k_compact(int64_t P, const uint32_t *__restrict__ touched,
-                                                          const uint32_t *__restrict__ dkey,
-                                                          const uint2 *__restrict__ rect, int tiles_x, int tile_bits,
-                                                          uint32_t *ok, uint32_t *ov, unsigned long long *lb,
-                                                          DevState *st) {
-    __shared__ unsigned s_w[10], s_tile;
-    __shared__ unsigned s_h[4 * 256];
-    __shared__ unsigned s_dlo[257], s_hhi[256], s_all;
-    const unsigned tag = epoch_tag(st, SLOT_COMPACT);
-    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    while (true) {
-        const unsigned tile = claim_tile(&st->ctr[SLOT_COMPACT], &s_tile);
-        const int64_t base = (int64_t)tile * kScanTile;
-        if (base >= P) break;
-        for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) s_h[i] = 0;
-        for (int i = threadIdx.x; i < 257; i += blockDim.x) s_dlo[i] = 0;
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_hhi[i] = 0;
-        if (threadIdx.x == 0) s_all = 0;
-        unsigned v[kScanItems], ex[kScanItems], tt[kScanItems];
-        const int64_t b0 = base + (int64_t)wid * 32 * kScanItems + lane;  // warp-striped
-#pragma unroll
-        for (int i = 0; i < kScanItems; i++) {
-            tt[i] = b0 + 32 * i < P ? touched[b0 + 32 * i] : 0u;
-            v[i] = tt[i] > 0 ? 1u : 0u;
-        }
-        unsigned total;
-        scan_lookback_striped<kScanItems>(v, ex, tile, lb, tag, s_w, total);
-#pragma unroll
-        for (int i = 0; i < kScanItems; i++) {
-            if (v[i]) {
-                const int64_t p = b0 + 32 * i;
-                const uint32_t k = dkey[p];
-                ok[ex[i]] = k;
-                ov[ex[i]] = (uint32_t)p;
-                const unsigned w = FULL ? tt[i] : 1u;
-#pragma unroll
-                for (int d = 0; d < 4; d++) atomicAdd(&s_h[d * 256 + ((k >> (8 * d)) & 255u)], w);
-                tile_digit_hist(rect[p], tiles_x, s_dlo, s_hhi, &s_all);
-            }
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
-            const unsigned h = s_h[i];
-            if (h) atomicAdd(&st->hist[HIST_DEPTH0][0] + i, h);
-        }
-        for (int i = threadIdx.x; i < 257; i += blockDim.x) {
-            const unsigned h = s_dlo[i];
-            if (h) atomicAdd(&st->tdlo[i], h);
-        }
-        if (tile_bits > 8)
-            for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-                const unsigned h = s_hhi[i];
-                if (h) atomicAdd(&st->hist[HIST_TILE0 + 1][i], h);
-            }
-        if (threadIdx.x == 0 && s_all) atomicAdd(&st->tdlo_all, s_all);
-        if (base + kScanTile >= P && threadIdx.x == 0) st->n_vis = total;
-    }
-}
-
-// Tile low-digit histogram from its difference array (one CTA of 256 threads).
-__global__ void k_tile_lo_hist(DevState *st) {
-    __shared__ unsigned s_ws[8];
-    const unsigned t = threadIdx.x, lane = t & 31, wid = t >> 5;
-    unsigned x = st->tdlo[t];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= (unsigned)o) x += y;
-    }
-    if (lane == 31) s_ws[wid] = x;
+    if (lane == 0) s_w[wid] = carry;
     __syncthreads();
-    unsigned add = 0;
-    for (unsigned w = 0; w < wid; w++) add += s_ws[w];
-    st->hist[HIST_TILE0][t] = x + add + st->tdlo_all;
+    unsigned pre = 0;
+    for (unsigned w = 0; w < wid; w++) pre = sat_add(pre, s_w[w]);
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) excl[i] = sat_add(pre, excl[i]);
 }
 
 // ----------------------------------------------------------------------------
@@ -317,75 +280,104 @@ __global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t *__re
                                                             const uint32_t *__restrict__ touched,
                                                             const uint2 *__restrict__ rect,
                                                             const uint32_t *__restrict__ dkey, int tiles_x,
-                                                            int64_t cap, void *tk_, uint32_t *tv,
-                                                            unsigned long long *lb, DevState *st) {
+                                                            int64_t cap, const uint32_t *__restrict__ doff,
+                                                            void *tk_, uint32_t *tv, DevState *st) {
     using Key = typename DupCfg<FULL>::Key;
     constexpr int CAP = DupCfg<FULL>::CAP;
     extern __shared__ __align__(16) unsigned char smem[];
     Key *s_k = reinterpret_cast<Key *>(smem);
     uint32_t *s_v = reinterpret_cast<uint32_t *>(s_k + CAP);
-    __shared__ unsigned s_w[10], s_tile, s_base;
+    __shared__ unsigned s_w[8], s_end;
+    __shared__ unsigned s_hl[256], s_hh[256];  // tile-digit histograms of this CTA's pairs
+    __shared__ unsigned s_hd[FULL ? 4 * 256 : 1];  // FULL: depth digits of the pair keys
     Key *tk = reinterpret_cast<Key *>(tk_);
-    const unsigned tag = epoch_tag(st, SLOT_DUP);
     const int64_t n = (int64_t)st->n_vis;
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    if (base >= n || st->overflow) return;
     const unsigned capu = (unsigned)(cap < 0xFFFFFFFFll ? cap : 0xFFFFFFFFll);
-    while (true) {
-        const unsigned tile = claim_tile(&st->ctr[SLOT_DUP], &s_tile);
-        const int64_t base = (int64_t)tile * kScanTile;
-        if (base >= n) break;
-        unsigned v[kScanItems], ex[kScanItems];
-        uint32_t id[kScanItems];
-        const int64_t b0 = base + (int64_t)(threadIdx.x >> 5) * 32 * kScanItems + (threadIdx.x & 31);  // warp-striped
+    unsigned v[kScanItems], ex[kScanItems];
+    uint32_t id[kScanItems];
+    const int64_t b0 = base + (int64_t)(threadIdx.x >> 5) * 32 * kScanItems + (threadIdx.x & 31);  // warp-striped
+#pragma unroll
+    for (int i = 0; i < kScanItems; i++) {
+        const bool in = b0 + 32 * i < n;
+        id[i] = in ? ids[b0 + 32 * i] : 0u;
+        v[i] = in ? touched[id[i]] : 0u;
+    }
+    block_scan_striped<kScanItems>(v, ex, s_w);
+    const unsigned pbase = doff[blockIdx.x];
+#pragma unroll
+    for (int i = 0; i < kScanItems; i++) ex[i] = sat_add(ex[i], pbase);
+    if (threadIdx.x == kScanThreads - 1) s_end = sat_add(ex[kScanItems - 1], v[kScanItems - 1]);
+    uint2 r[kScanItems];
+    uint32_t dk[kScanItems];
+#pragma unroll
+    for (int i = 0; i < kScanItems; i++) {
+        r[i] = v[i] ? rect[id[i]] : make_uint2(0u, 0u);
+        dk[i] = (FULL && v[i]) ? dkey[id[i]] : 0u;
+    }
+    __syncthreads();
+    const unsigned pend = min(s_end, capu);
+    for (int i = threadIdx.x; i < 256; i += kScanThreads) s_hl[i] = s_hh[i] = 0;
+    if (FULL)
+        for (int i = threadIdx.x; i < 4 * 256; i += kScanThreads) s_hd[FULL ? i : 0] = 0;
+    for (unsigned wb = pbase; wb < pend; wb += CAP) {
+        const unsigned we = min(pend, wb + CAP);
 #pragma unroll
         for (int i = 0; i < kScanItems; i++) {
-            const bool in = b0 + 32 * i < n;
-            id[i] = in ? ids[b0 + 32 * i] : 0u;
-            v[i] = in ? touched[id[i]] : 0u;
-        }
-        unsigned total;
-        scan_lookback_striped<kScanItems>(v, ex, tile, lb, tag, s_w, total);
-        if (threadIdx.x == 0) s_base = ex[0];
-        uint2 r[kScanItems];
-        uint32_t dk[kScanItems];
-#pragma unroll
-        for (int i = 0; i < kScanItems; i++) {
-            r[i] = v[i] ? rect[id[i]] : make_uint2(0u, 0u);
-            dk[i] = (FULL && v[i]) ? dkey[id[i]] : 0u;
+            if (!v[i]) continue;
+            const unsigned lo = max(ex[i], wb), hi = min(sat_add(ex[i], v[i]), we);
+            if (lo >= hi) continue;
+            const unsigned x0 = r[i].x & 0xFFFF, y0 = r[i].x >> 16, x1 = r[i].y & 0xFFFF;
+            const unsigned wdt = x1 - x0 + 1, l0 = lo - ex[i];
+            unsigned tx = x0 + l0 % wdt, ty = y0 + l0 / wdt;
+            for (unsigned g = lo; g < hi; g++) {
+                const unsigned t = ty * (unsigned)tiles_x + tx;
+                if (FULL) s_k[g - wb] = (Key)(((unsigned long long)t << 32) | dk[i]);
+                else s_k[g - wb] = (Key)t;
+                s_v[g - wb] = id[i];
+                if (++tx > x1) { tx = x0; ty++; }
+            }
         }
         __syncthreads();
-        const unsigned pbase = s_base, pend = min(total, capu);
-        for (unsigned wb = pbase; wb < pend; wb += CAP) {
-            const unsigned we = min(pend, wb + CAP);
+        for (unsigned k = threadIdx.x; k < we - wb; k += kScanThreads) {
+            tk[wb + k] = s_k[k];
+            tv[wb + k] = s_v[k];
+        }
+        // tile-digit histograms over contiguous segments of the window: the low
+        // digit of consecutive pairs varies (one atomic each, spread bins), the high
+        // digit runs (one atomic per run)
+        {
+            const unsigned nw = we - wb, seg = (nw + kScanThreads - 1) / kScanThreads;
+            const unsigned k0 = threadIdx.x * seg, k1 = min(nw, k0 + seg);
+            unsigned run_v = 0xFFFFFFFFu, run_n = 0;
+            for (unsigned k = k0; k < k1; k++) {
+                const unsigned t = FULL ? (unsigned)((unsigned long long)s_k[k] >> 32) : (unsigned)s_k[k];
+                atomicAdd(&s_hl[t & 255u], 1u);
+                if (FULL) {
+                    const unsigned long long kk = (unsigned long long)s_k[k];
 #pragma unroll
-            for (int i = 0; i < kScanItems; i++) {
-                if (!v[i]) continue;
-                const unsigned lo = max(ex[i], wb), hi = min(ex[i] + v[i], we);
-                if (lo >= hi) continue;
-                const unsigned x0 = r[i].x & 0xFFFF, y0 = r[i].x >> 16, x1 = r[i].y & 0xFFFF;
-                const unsigned wdt = x1 - x0 + 1, l0 = lo - ex[i];
-                unsigned tx = x0 + l0 % wdt, ty = y0 + l0 / wdt;
-                for (unsigned g = lo; g < hi; g++) {
-                    const unsigned t = ty * (unsigned)tiles_x + tx;
-                    if (FULL) s_k[g - wb] = (Key)(((unsigned long long)t << 32) | dk[i]);
-                    else s_k[g - wb] = (Key)t;
-                    s_v[g - wb] = id[i];
-                    if (++tx > x1) { tx = x0; ty++; }
+                    for (int d = 0; d < 4; d++) atomicAdd(&s_hd[d * 256 + ((unsigned)(kk >> (8 * d)) & 255u)], 1u);
                 }
+                const unsigned h = (t >> 8) & 255u;
+                if (h != run_v) {
+                    if (run_n) atomicAdd(&s_hh[run_v], run_n);
+                    run_v = h;
+                    run_n = 0;
+                }
+                run_n++;
             }
-            __syncthreads();
-            for (unsigned k = threadIdx.x; k < we - wb; k += kScanThreads) {
-                tk[wb + k] = s_k[k];
-                tv[wb + k] = s_v[k];
-            }
-            __syncthreads();
+            if (run_n) atomicAdd(&s_hh[run_v], run_n);
         }
-        if (base + kScanTile >= n && threadIdx.x == 0) {
-            st->needed = total;
-            const bool over = (int64_t)total > cap;
-            st->overflow = over ? 1u : 0u;
-            st->K = over ? 0u : total;
-        }
+        __syncthreads();
     }
+    for (int i = threadIdx.x; i < 256; i += kScanThreads) {
+        if (s_hl[i]) atomicAdd(&st->hist[FULL ? 4 : HIST_TILE0][i], s_hl[i]);
+        if (s_hh[i]) atomicAdd(&st->hist[FULL ? 5 : HIST_TILE0 + 1][i], s_hh[i]);
+    }
+    if (FULL)
+        for (int i = threadIdx.x; i < 4 * 256; i += kScanThreads)
+            if (s_hd[FULL ? i : 0]) atomicAdd(&st->hist[i / 256][i % 256], s_hd[FULL ? i : 0]);
 }
 
 // ----------------------------------------------------------------------------
@@ -662,26 +654,21 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
     const int tb = bits_for(tiles);
     const bool full = sort_mode == 1;
     cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * (size_t)tiles, s);
-    const int scan_grid =
-        (int)std::max<int64_t>(1, std::min<int64_t>((P + kScanTile - 1) / kScanTile, (int64_t)sm_count * 8));
+    // compaction of the visible primitives (B2 then B1 CTA counts)
+    const int nbt = (int)((F + 255) / 256), nbg = (int)((N + 255) / 256);
     if (P > 0) {
-        if (full)
-            k_compact<true><<<scan_grid, kScanThreads, 0, s>>>(P, b.touched, b.dkey, b.rect, cam.tiles_x, tb, b.pk[0],
-                                                               b.pv[0], b.lookback, b.st);
-        else
-            k_compact<false><<<scan_grid, kScanThreads, 0, s>>>(P, b.touched, b.dkey, b.rect, cam.tiles_x, tb, b.pk[0],
-                                                                b.pv[0], b.lookback, b.st);
-        launches++;
+        k_scan_counts<<<1, 1024, 0, s>>>(b.bcnt, nbt + nbg, 0, 0, b.st);
+        k_compact<<<nbt + nbg, 256, 0, s>>>(F, N, nbt, b.touched, b.dkey, b.bcnt, b.pk[0], b.pv[0]);
+        launches += 2;
     }
-    k_tile_lo_hist<<<1, 256, 0, s>>>(b.st);
-    launches++;
     int slot = SLOT_PASS0;
-    const int dgrid =
-        (int)std::max<int64_t>(1, std::min<int64_t>((P + kScanTile - 1) / kScanTile, (int64_t)sm_count * 4));
-    const int g2 = sort_grid(b.max_pairs, sm_count, 2);
+    const int dgrid = (int)std::max<int64_t>(1, (P + kScanTile - 1) / kScanTile);
     int tc = 0;
+    const uint32_t *dup_ids;
     if (!full) {
         // depth sort of the visible primitives
+        k_hist_depth<<<sm_count * 2, 256, 0, s>>>(b.pk[0], b.st);
+        launches++;
         const int g1 = sort_grid(P, sm_count, 2);
         int cur = 0;
         for (int pass = 0; pass < 4; pass++, slot++) {
@@ -690,9 +677,19 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
             cur ^= 1;
             launches++;
         }
-        k_duplicate<false><<<dgrid, kScanThreads, dup_smem<false>(), s>>>(b.pv[cur], b.touched, b.rect, b.dkey,
-                                                                          cam.tiles_x, b.max_pairs, b.tk[0], b.tv[0],
-                                                                          b.lookback, b.st);
+        dup_ids = b.pv[cur];
+    } else {
+        dup_ids = b.pv[0];
+    }
+    // pair counts per run of kScanTile primitives -> scan (K, capacity) -> emission
+    k_dup_count<<<dgrid, kScanThreads, 0, s>>>(dup_ids, b.touched, b.dcnt, b.st);
+    k_scan_counts<<<1, 1024, 0, s>>>(b.dcnt, dgrid, 1, b.max_pairs, b.st);
+    launches += 2;
+    const int g2 = sort_grid(b.max_pairs, sm_count, 2);
+    if (!full) {
+        k_duplicate<false><<<dgrid, kScanThreads, dup_smem<false>(), s>>>(dup_ids, b.touched, b.rect, b.dkey,
+                                                                          cam.tiles_x, b.max_pairs, b.dcnt, b.tk[0],
+                                                                          b.tv[0], b.st);
         launches++;
         for (int pass = 0, sh = 0; sh < tb; pass++, sh += 8, slot++) {
             onesweep_pass<uint16_t>(b, (const uint16_t *)b.tk[tc], b.tv[tc], (uint16_t *)b.tk[tc ^ 1], b.tv[tc ^ 1],
@@ -704,8 +701,8 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         k_ranges16<<<sm_count * 4, 256, 0, s>>>((const uint16_t *)b.tk[tc], &b.st->K, b.ranges, b.st);
         launches++;
     } else {
-        k_duplicate<true><<<dgrid, kScanThreads, dup_smem<true>(), s>>>(b.pv[0], b.touched, b.rect, b.dkey, cam.tiles_x,
-                                                                        b.max_pairs, b.tk[0], b.tv[0], b.lookback, b.st);
+        k_duplicate<true><<<dgrid, kScanThreads, dup_smem<true>(), s>>>(dup_ids, b.touched, b.rect, b.dkey, cam.tiles_x,
+                                                                        b.max_pairs, b.dcnt, b.tk[0], b.tv[0], b.st);
         launches++;
         const int total_bits = 32 + tb;
         for (int pass = 0, sh = 0; sh < total_bits; pass++, sh += 8, slot++) {

@@ -37,6 +37,20 @@ int launch_begin_frame(DevState *st, cudaStream_t s) {
     return 1;
 }
 
+// Count of `flag` over the CTA (256 threads) written to *out by thread 0 (the
+// per-CTA visible counts the compaction scans; no atomics, no look-back).
+__device__ __forceinline__ void block_count(bool flag, unsigned *out) {
+    __shared__ unsigned s_c[8];
+    const unsigned c = __popc(__ballot_sync(0xffffffffu, flag));
+    if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t = 0;
+        for (unsigned w = 0; w < (blockDim.x >> 5); w++) t += s_c[w];
+        *out = t;
+    }
+}
+
 // 3DGS real SH basis, fp32
 __device__ __forceinline__ void sh_eval(const float *__restrict__ sh, int deg, float x, float y, float z, float out[3]) {
     const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
@@ -210,6 +224,7 @@ __global__ void __launch_bounds__(256) k_preprocess_gaussians(GaussInput gin, in
     }
     const unsigned cnt = __popc(__ballot_sync(0xffffffffu, vis));
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&b.st->vis_g, cnt);
+    block_count(vis, b.bcnt + (F + 255) / 256 + blockIdx.x);
 }
 
 int launch_preprocess_gaussians(const GaussInput &g, int64_t F, const CamParams &cam, float dilation,
@@ -312,6 +327,7 @@ __global__ void __launch_bounds__(256) k_setup_triangles(MeshInput m, CamParams 
         if (cv) atomicAdd(&b.st->vis_t, cv);
         if (cg) atomicAdd(&b.st->culled_guard, cg);
     }
+    block_count(vis, b.bcnt + blockIdx.x);
 }
 
 int launch_setup_triangles(const MeshInput &m, const CamParams &cam, const Buffers &b, cudaStream_t s) {
