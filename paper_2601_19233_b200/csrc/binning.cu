@@ -387,7 +387,6 @@ __global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t *__re
 // position BEFORE the per-digit decoupled look-back (so no key register is live
 // across it); then a coalesced-by-digit scatter to global memory.
 // ----------------------------------------------------------------------------
-template <typename KT>
 #ifndef UNIMGS_RANK_MATCH
 #define UNIMGS_RANK_MATCH 0
 #endif
@@ -397,11 +396,13 @@ template <typename KT>
 #ifndef UNIMGS_SORT_MINB
 #define UNIMGS_SORT_MINB 2
 #endif
-__global__ void __launch_bounds__(kSortThreads, UNIMGS_SORT_MINB) k_onesweep(const KT *__restrict__ kin,
+template <typename KT, int ITEMS>
+__global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MINB)) k_onesweep(const KT *__restrict__ kin,
                                                               const uint32_t *__restrict__ vin, KT *__restrict__ kout,
                                                               uint32_t *__restrict__ vout, const unsigned *n_ptr,
                                                               int shift, int bits, const unsigned *hist, int slot,
                                                               unsigned long long *lb, DevState *st) {
+    constexpr int TILE_ = kSortThreads * ITEMS;
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned *s_wh = reinterpret_cast<unsigned *>(smem);           // [8][256]
     unsigned *s_doff = s_wh + 8 * 256;                              // [256] block-local digit offsets
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(kSortThreads, UNIMGS_SORT_MINB) k_onesweep(con
     unsigned *s_hex = reinterpret_cast<unsigned *>(s_glob + 256);   // [256] global exclusive histogram
     unsigned *s_misc = s_hex + 256;                                 // [16]
     KT *s_k = reinterpret_cast<KT *>(s_misc + 16);
-    uint32_t *s_v = reinterpret_cast<uint32_t *>(s_k + kSortTile);
+    uint32_t *s_v = reinterpret_cast<uint32_t *>(s_k + TILE_);
 
     const unsigned n = *n_ptr;
     const unsigned tag = epoch_tag(st, slot);
@@ -434,26 +435,26 @@ __global__ void __launch_bounds__(kSortThreads, UNIMGS_SORT_MINB) k_onesweep(con
 
     while (true) {
         const unsigned tile = claim_tile(&st->ctr[slot], &s_misc[1]);
-        if ((unsigned long long)tile * kSortTile >= n) break;
-        const unsigned base = tile * (unsigned)kSortTile;
+        if ((unsigned long long)tile * TILE_ >= n) break;
+        const unsigned base = tile * (unsigned)TILE_;
         for (int i = t; i < 8 * 256; i += kSortThreads) s_wh[i] = 0;
         __syncthreads();
 
-        KT key[kSortItems];
-        uint32_t val[kSortItems];
-        unsigned rank[kSortItems];
-        const unsigned wbase = base + wid * 32u * kSortItems + lane;
+        KT key[ITEMS];
+        uint32_t val[ITEMS];
+        unsigned rank[ITEMS];
+        const unsigned wbase = base + wid * 32u * ITEMS + lane;
         const unsigned lt = lanemask_lt();
         unsigned *wh = s_wh + wid * 256;
 #pragma unroll
-        for (int i = 0; i < kSortItems; i++) {
+        for (int i = 0; i < ITEMS; i++) {
             const unsigned idx = wbase + 32u * i;
             const bool valid = idx < n;
             key[i] = valid ? kin[idx] : (KT)0;
             val[i] = valid ? vin[idx] : 0u;
         }
 #pragma unroll
-        for (int i = 0; i < kSortItems; i++) {
+        for (int i = 0; i < ITEMS; i++) {
             // stable warp multisplit: the lanes holding the same digit
             const bool valid = wbase + 32u * i < n;
             const unsigned d = valid ? (unsigned)((key[i] >> shift) & mask) : 0u;
@@ -512,7 +513,7 @@ __global__ void __launch_bounds__(kSortThreads, UNIMGS_SORT_MINB) k_onesweep(con
         __syncthreads();
         // keys into shared memory at their block-sorted position
 #pragma unroll
-        for (int i = 0; i < kSortItems; i++) {
+        for (int i = 0; i < ITEMS; i++) {
             if (wbase + 32u * i < n) {
                 const unsigned d = (unsigned)((key[i] >> shift) & mask);
                 const unsigned pos = s_doff[d] + wh[d] + rank[i];
@@ -547,7 +548,7 @@ __global__ void __launch_bounds__(kSortThreads, UNIMGS_SORT_MINB) k_onesweep(con
         }
         s_glob[t] = (int)(s_hex[t] + excl) - (int)s_doff[t];
         __syncthreads();
-        const unsigned nt = min((unsigned)kSortTile, n - base);
+        const unsigned nt = min((unsigned)TILE_, n - base);
         for (unsigned k = t; k < nt; k += kSortThreads) {
             const KT kk = s_k[k];
             const unsigned d = (unsigned)((kk >> shift) & mask);
@@ -604,10 +605,14 @@ __global__ void k_ranges64(const unsigned long long *__restrict__ keys, const un
     }
 }
 
-template <typename KT>
+template <typename KT, int ITEMS>
 static size_t onesweep_smem() {
-    return (8 * 256 + 256 * 3 + 16) * sizeof(unsigned) + kSortTile * (sizeof(KT) + sizeof(uint32_t));
+    return (8 * 256 + 256 * 3 + 16) * sizeof(unsigned) + kSortThreads * ITEMS * (sizeof(KT) + sizeof(uint32_t));
 }
+#ifndef UNIMGS_DEPTH_ITEMS
+#define UNIMGS_DEPTH_ITEMS 8
+#endif
+constexpr int kDepthItems = UNIMGS_DEPTH_ITEMS;  // small depth sort: short tiles, latency-bound
 
 template <bool FULL>
 static size_t dup_smem() {
@@ -620,26 +625,28 @@ static int bits_for(int64_t tiles) {
     return b;
 }
 
-template <typename KT>
+template <typename KT, int ITEMS = kSortItems>
 static void onesweep_pass(Buffers &b, const KT *kin, const uint32_t *vin, KT *kout, uint32_t *vout,
                           const unsigned *n_ptr, int shift, int bits, int hist_row, int slot, int grid,
                           cudaStream_t s) {
-    k_onesweep<KT><<<grid, kSortThreads, onesweep_smem<KT>(), s>>>(kin, vin, kout, vout, n_ptr, shift, bits,
-                                                                  &b.st->hist[hist_row][0], slot, b.lookback, b.st);
+    k_onesweep<KT, ITEMS><<<grid, kSortThreads, onesweep_smem<KT, ITEMS>(), s>>>(
+        kin, vin, kout, vout, n_ptr, shift, bits, &b.st->hist[hist_row][0], slot, b.lookback, b.st);
 }
 
-static int sort_grid(int64_t max_items, int sm_count, int per_sm) {
-    const int64_t tiles = (max_items + kSortTile - 1) / kSortTile;
+static int sort_grid(int64_t max_items, int sm_count, int per_sm, int tile = kSortTile) {
+    const int64_t tiles = (max_items + tile - 1) / tile;
     return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count * per_sm));
 }
 
 static void set_attrs() {
     static bool done = false;
     if (done) return;
-    cudaFuncSetAttribute(k_onesweep<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)onesweep_smem<uint16_t>());
-    cudaFuncSetAttribute(k_onesweep<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)onesweep_smem<uint32_t>());
-    cudaFuncSetAttribute(k_onesweep<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)onesweep_smem<unsigned long long>());
+    cudaFuncSetAttribute(k_onesweep<uint16_t, kSortItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)onesweep_smem<uint16_t, kSortItems>());
+    cudaFuncSetAttribute(k_onesweep<uint32_t, kDepthItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)onesweep_smem<uint32_t, kDepthItems>());
+    cudaFuncSetAttribute(k_onesweep<unsigned long long, kSortItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)onesweep_smem<unsigned long long, kSortItems>());
     cudaFuncSetAttribute(k_duplicate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dup_smem<false>());
     cudaFuncSetAttribute(k_duplicate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dup_smem<true>());
     done = true;
@@ -669,11 +676,11 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         // depth sort of the visible primitives
         k_hist_depth<<<sm_count * 2, 256, 0, s>>>(b.pk[0], b.st);
         launches++;
-        const int g1 = sort_grid(P, sm_count, 2);
+        const int g1 = sort_grid(P, sm_count, kDepthItems <= 4 ? 4 : 2, kSortThreads * kDepthItems);
         int cur = 0;
         for (int pass = 0; pass < 4; pass++, slot++) {
-            onesweep_pass<uint32_t>(b, b.pk[cur], b.pv[cur], b.pk[cur ^ 1], b.pv[cur ^ 1], &b.st->n_vis, 8 * pass, 8,
-                                    HIST_DEPTH0 + pass, slot, g1, s);
+            onesweep_pass<uint32_t, kDepthItems>(b, b.pk[cur], b.pv[cur], b.pk[cur ^ 1], b.pv[cur ^ 1], &b.st->n_vis,
+                                                 8 * pass, 8, HIST_DEPTH0 + pass, slot, g1, s);
             cur ^= 1;
             launches++;
         }

@@ -8,7 +8,7 @@
 #include "../../paper_2601_19233_b200/csrc/binning.cu"
 using namespace unimgs;
 
-template <typename KT>
+template <typename KT, int ITEMS>
 static float run(int n, int bits, int reps, bool check) {
     std::vector<KT> hk(n);
     std::vector<uint32_t> hv(n);
@@ -36,8 +36,8 @@ static float run(int n, int bits, int reps, bool check) {
         cudaEventRecord(e0);
         int c = 0, slot = 2;
         for (int p = 0, sh = 0; sh < bits; p++, sh += 8, slot++) {
-            onesweep_pass<KT>(b, k[c], v[c], k[c ^ 1], v[c ^ 1], &st->K, sh, std::min(8, bits - sh), p, slot,
-                              sort_grid(n, sms, 2), 0);
+            onesweep_pass<KT, ITEMS>(b, k[c], v[c], k[c ^ 1], v[c ^ 1], &st->K, sh, std::min(8, bits - sh), p, slot,
+                              sort_grid(n, sms, ITEMS <= 4 ? 4 : 2, 256 * ITEMS), 0);
             c ^= 1;
         }
         cudaEventRecord(e1); cudaEventSynchronize(e1);
@@ -54,14 +54,14 @@ static float run(int n, int bits, int reps, bool check) {
             printf("  check %s\n", good ? "OK" : "FAILED");
         }
     }
-    printf("%s n=%d bits=%d: %.1f us (%.2f GB/s per pass moved)\n", sizeof(KT) == 2 ? "u16" : "u32", n, bits,
+    printf("%s items=%d n=%d bits=%d: %.1f us (%.2f GB/s per pass moved)\n", sizeof(KT) == 2 ? "u16" : "u32", ITEMS, n, bits,
            best * 1e3, (double)n * (2 * sizeof(KT) + 8) * ((bits + 7) / 8) / (best * 1e-3) / 1e9);
     return best;
 }
 
 int main() {
-    run<uint16_t>(7480746, 13, 5, true);
-    run<uint32_t>(1551224, 32, 5, true);
-    run<uint32_t>(1551224, 16, 5, false);
+    run<uint16_t, kSortItems>(7480746, 13, 5, true);
+    run<uint32_t, kDepthItems>(1551224, 32, 5, true);
+    run<uint32_t, kSortItems>(1551224, 32, 5, false);
     return 0;
 }
