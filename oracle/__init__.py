@@ -40,7 +40,11 @@ class CCamera(C.Structure):
 
 class CSettings(C.Structure):
     _fields_ = [("alpha_max", C.c_float), ("t_eps", C.c_float), ("dilation", C.c_float),
-                ("bg", C.c_float * 3), ("bg_alpha", C.c_float)]
+                ("bg", C.c_float * 3), ("bg_alpha", C.c_float), ("blend_mode", C.c_int32), ("msaa", C.c_int32)]
+
+
+# blend modes: the paper's ablation (Fig.3 / Fig.4)
+EXACT, NAIVE, MSAA_PIXEL, WHOLE_PIXEL, PAPER_LITERAL = range(5)
 
 
 class CFrag(C.Structure):
@@ -86,6 +90,10 @@ def lib():
         L.or_get_bins.argtypes = [vp, vp, vp, vp]
         L.or_coverage_mask.argtypes = [vp, i32, i32]
         L.or_coverage_mask.restype = C.c_uint32
+        L.or_coverage_mask_m.argtypes = [vp, i32, i32, i32]
+        L.or_coverage_mask_m.restype = C.c_uint32
+        L.or_render_supersampled.argtypes = [vp, vp, i32, i32]
+        L.or_render_supersampled.restype = i32
         L.or_sh_basis_colour.argtypes = [vp, i32, vp, vp]
         _lib = L
     return _lib
@@ -95,9 +103,11 @@ def _ptr(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data
 
 
-def make_settings(alpha_max=0.99, t_eps=1e-4, dilation=0.3, bg=(0.0, 0.0, 0.0), bg_alpha=1.0) -> CSettings:
+def make_settings(alpha_max=0.99, t_eps=1e-4, dilation=0.3, bg=(0.0, 0.0, 0.0), bg_alpha=1.0, blend_mode=EXACT,
+                  msaa=4) -> CSettings:
     s = CSettings()
     s.alpha_max, s.t_eps, s.dilation, s.bg_alpha = alpha_max, t_eps, dilation, bg_alpha
+    s.blend_mode, s.msaa = blend_mode, msaa
     for i in range(3):
         s.bg[i] = float(bg[i])
     return s
@@ -217,6 +227,14 @@ class Oracle:
                 return buf[:n]
             cap = int(n)
 
+    def render_supersampled(self, S: int = 16) -> np.ndarray:
+        """Ground truth: mean of S x S sub-samples of exact per-sample ordered blending."""
+        H, W = self.cam.height, self.cam.width
+        out = np.zeros((H, W, 4), np.float64)
+        if lib().or_render_supersampled(self._h, _ptr(out), S, self.threads):
+            raise RuntimeError("supersampled render needs project() and 256 % S == 0")
+        return out
+
     def support_truncation(self) -> int:
         return int(lib().or_support_truncation(self._h))
 
@@ -253,6 +271,11 @@ def frags(*items) -> np.ndarray:
 def coverage_mask(xy6, x: int, y: int) -> int:
     xy = np.ascontiguousarray(xy6, np.int32)
     return int(lib().or_coverage_mask(_ptr(xy), x, y))
+
+
+def coverage_mask_m(xy6, x: int, y: int, M: int) -> int:
+    xy = np.ascontiguousarray(xy6, np.int32)
+    return int(lib().or_coverage_mask_m(_ptr(xy), x, y, M))
 
 
 def sh_colour(coef: np.ndarray, degree: int, direction) -> np.ndarray:

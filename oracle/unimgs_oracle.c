@@ -35,7 +35,10 @@
 #endif
 
 #define OR_TILE 16
-#define OR_M 4
+#define OR_MMAX 16
+
+/* blend modes (the paper's ablation Fig.3 / Fig.4) */
+enum { OR_EXACT = 0, OR_NAIVE = 1, OR_MSAA_PIXEL = 2, OR_WHOLE_PIXEL = 3, OR_PAPER_LITERAL = 4 };
 
 typedef struct {
     int32_t width, height;
@@ -48,6 +51,8 @@ typedef struct {
     float alpha_max, t_eps, dilation;
     float bg[3];
     float bg_alpha;
+    int32_t blend_mode; /* OR_EXACT .. OR_PAPER_LITERAL */
+    int32_t msaa;       /* M in {1, 2, 4, 8, 16} (P:330 uses 4) */
 } or_settings;
 
 typedef struct {
@@ -428,9 +433,26 @@ int64_t or_bin(or_ctx *c) {
 /* ------------------------------------------------------------------------- */
 /* Fragment evaluation at pixel (x, y).                                         */
 
-/* D3D standard 4x pattern in 1/16 px (R10) */
-static const int OR_SX[OR_M] = {-2, 6, -6, 2};
-static const int OR_SY[OR_M] = {-6, -2, 2, 6};
+/* Direct3D standard multisample patterns in 1/16 px from the pixel centre (R10);
+ * M = 4 is the paper's setting. */
+static const int OR_PAT1[1][2] = {{0, 0}};
+static const int OR_PAT2[2][2] = {{4, 4}, {-4, -4}};
+static const int OR_PAT4[4][2] = {{-2, -6}, {6, -2}, {-6, 2}, {2, 6}};
+static const int OR_PAT8[8][2] = {{1, -3}, {-1, 3}, {5, 1}, {-3, -5}, {-5, 5}, {-7, -1}, {3, 7}, {7, -7}};
+static const int OR_PAT16[16][2] = {{1, 1}, {-1, -3}, {-3, 2}, {4, -1}, {-5, -2}, {2, 5}, {5, 3}, {3, -5},
+                                    {-2, 6}, {0, -7}, {-4, -6}, {-6, 4}, {-8, 0}, {7, -4}, {6, 7}, {-7, -8}};
+
+static const int (*or_pattern(int M))[2] {
+    switch (M) {
+        case 1: return OR_PAT1;
+        case 2: return OR_PAT2;
+        case 8: return OR_PAT8;
+        case 16: return OR_PAT16;
+        default: return OR_PAT4;
+    }
+}
+
+static int or_msaa(const or_settings *s) { return (s->msaa == 1 || s->msaa == 2 || s->msaa == 8 || s->msaa == 16) ? s->msaa : 4; }
 
 /* N6: q at the pixel centre; fragment iff q <= q_max (equivalent to alpha >= 1/255) */
 static int gaussian_fragment(const or_ctx *c, int64_t g, int x, int y, or_frag *fr) {
@@ -463,11 +485,28 @@ static int edge_inclusive(const int32_t *xy, int k) {
     return dy > 0 || (dy == 0 && dx < 0);
 }
 
+/* point (PX, PY) in 1/256 px inside the oriented triangle, top-left-style rule (N7, R11) */
+static int or_inside(const int32_t *xy, int64_t PX, int64_t PY) {
+    for (int k = 0; k < 3; k++) {
+        int64_t e = edge_fn(xy, k, PX, PY);
+        if (e < (edge_inclusive(xy, k) ? 0 : 1)) return 0;
+    }
+    return 1;
+}
+
+uint32_t or_coverage_mask_m(const int32_t *xy, int x, int y, int M) {
+    const int (*pat)[2] = or_pattern(M);
+    uint32_t m = 0;
+    for (int j = 0; j < M; j++)
+        if (or_inside(xy, 256 * (int64_t)x + 128 + 16 * pat[j][0], 256 * (int64_t)y + 128 + 16 * pat[j][1])) m |= 1u << j;
+    return m;
+}
+
 uint32_t or_coverage_mask(const int32_t *xy, int x, int y) {
     uint32_t m = 0;
-    for (int j = 0; j < OR_M; j++) {
-        int64_t PX = 256 * (int64_t)x + 128 + 16 * OR_SX[j];
-        int64_t PY = 256 * (int64_t)y + 128 + 16 * OR_SY[j];
+    for (int j = 0; j < 4; j++) {
+        int64_t PX = 256 * (int64_t)x + 128 + 16 * OR_PAT4[j][0];
+        int64_t PY = 256 * (int64_t)y + 128 + 16 * OR_PAT4[j][1];
         int in = 1;
         for (int k = 0; k < 3; k++) {
             int64_t e = edge_fn(xy, k, PX, PY);
@@ -486,12 +525,11 @@ static double texel(const or_ctx *c, int64_t i, int64_t j, int ch) {
     return (double)c->tex[(j * c->tw + i) * 4 + ch] / 255.0;
 }
 
-/* Triangle colour at the pixel centre (R12): perspective-correct, unclamped barycentrics. */
-static void triangle_colour(const or_ctx *c, int64_t f, int x, int y, double rgb[3]) {
+/* Triangle colour at (PX, PY) in 1/256 px: perspective-correct, unclamped barycentrics (R12). */
+static void triangle_colour_at(const or_ctx *c, int64_t f, int64_t PX, int64_t PY, double rgb[3]) {
     const int32_t *xy = c->t_xy + 6 * f;
     const int32_t *vid = c->t_vid + 3 * f;
     const float *tz = c->t_z + 3 * f;
-    int64_t PX = 256 * (int64_t)x + 128, PY = 256 * (int64_t)y + 128;
     int64_t A2 = (int64_t)(xy[2] - xy[0]) * (xy[5] - xy[1]) - (int64_t)(xy[4] - xy[0]) * (xy[3] - xy[1]);
     double b[3], w[3], sw = 0.0, lam[3];
     for (int k = 0; k < 3; k++) {
@@ -531,9 +569,14 @@ static void triangle_colour(const or_ctx *c, int64_t f, int x, int y, double rgb
     }
 }
 
+/* at the pixel centre (R12) */
+static void triangle_colour(const or_ctx *c, int64_t f, int x, int y, double rgb[3]) {
+    triangle_colour_at(c, f, 256 * (int64_t)x + 128, 256 * (int64_t)y + 128, rgb);
+}
+
 static int triangle_fragment(const or_ctx *c, int64_t f, int x, int y, or_frag *fr) {
     if (!c->t_touched[f]) return 0;
-    uint32_t m = or_coverage_mask(c->t_xy + 6 * f, x, y);
+    uint32_t m = or_coverage_mask_m(c->t_xy + 6 * f, x, y, or_msaa(&c->set));
     if (!m) return 0;
     fr->id = (uint32_t)f;
     fr->kind = 1;
@@ -552,48 +595,89 @@ static int triangle_fragment(const or_ctx *c, int64_t f, int x, int y, or_frag *
  *   exit T = T_e * mean_j t^j (R3); out = C + T * bg_alpha * C_bg (R5);
  *   blend-then-test termination T_eff < t_eps (R16).                          */
 typedef struct {
-    double C[3], T, Te, t[OR_M], Teff;
-    int open, done;
+    double C[3], T, Te, t[OR_MMAX], Teff;
+    double G;   /* OR_WHOLE_PIXEL: Gaussian attenuation since the entity opened */
+    double Tl;  /* OR_PAPER_LITERAL: pixel T updated per triangle by Eq.6 (geometric O) */
+    int open, done, M, mode;
 } or_pix;
 
-static void pix_init(or_pix *s) {
+static void pix_init(or_pix *s, const or_settings *set) {
     memset(s, 0, sizeof(*s));
     s->T = 1.0;
     s->Teff = 1.0;
+    s->M = or_msaa(set);
+    s->mode = set->blend_mode;
 }
 
 static double mean_t(const or_pix *s) {
     double a = 0.0;
-    for (int j = 0; j < OR_M; j++) a += s->t[j];
-    return a / OR_M;
+    for (int j = 0; j < s->M; j++) a += s->t[j];
+    return a / s->M;
+}
+
+static double popc_frac(const or_pix *s, uint32_t m) {
+    int n = 0;
+    for (int j = 0; j < s->M; j++) n += (m >> j) & 1u;
+    return (double)n / s->M;
+}
+
+/* The entity's exit transmittance under the active mode. */
+static double exit_T(const or_pix *s) {
+    if (s->mode == OR_PAPER_LITERAL) return s->Tl;
+    if (s->mode == OR_WHOLE_PIXEL) return s->Te * mean_t(s) * s->G;
+    return s->Te * mean_t(s); /* R3 */
 }
 
 static void pix_apply(or_pix *s, const or_frag *fr, const or_settings *set) {
+    const int mode = s->mode;
     if (fr->kind == 0) {
-        if (s->open) { s->T = s->Te * mean_t(s); s->open = 0; }
+        if (mode == OR_WHOLE_PIXEL && s->open) {
+            /* Fig.3b/c: one entity spans the whole list; the Gaussian blends with the current
+             * transmittance but does not attenuate the entity's sub-pixel state */
+            double Tn = s->Te * mean_t(s) * s->G;
+            for (int k = 0; k < 3; k++) s->C[k] += Tn * fr->alpha * fr->rgb[k];
+            s->G *= (1.0 - fr->alpha);
+            s->Teff = s->Te * mean_t(s) * s->G;
+        } else {
+            if (s->open) { s->T = exit_T(s); s->open = 0; } /* depth-adjacency broken */
+            for (int k = 0; k < 3; k++) s->C[k] += s->T * fr->alpha * fr->rgb[k];
+            s->T = s->T * (1.0 - fr->alpha);
+            s->Teff = s->T;
+        }
+    } else if (mode == OR_NAIVE) {
+        /* Fig.3a / 4a: a triangle fragment blends like a Gaussian at full coverage */
         for (int k = 0; k < 3; k++) s->C[k] += s->T * fr->alpha * fr->rgb[k];
         s->T = s->T * (1.0 - fr->alpha);
+        s->Teff = s->T;
+    } else if (mode == OR_MSAA_PIXEL) {
+        /* Eq.5-6: geometric coverage, pixel-level transmittance */
+        double O = popc_frac(s, fr->mask);
+        for (int k = 0; k < 3; k++) s->C[k] += s->T * O * fr->alpha * fr->rgb[k];
+        s->T = s->T * (1.0 - O * fr->alpha);
         s->Teff = s->T;
     } else {
         if (!s->open) {
             s->open = 1;
             s->Te = s->T;
-            for (int j = 0; j < OR_M; j++) s->t[j] = 1.0;
+            s->G = 1.0;
+            s->Tl = s->T;
+            for (int j = 0; j < s->M; j++) s->t[j] = 1.0;
         }
         double O = 0.0;
-        for (int j = 0; j < OR_M; j++)
+        for (int j = 0; j < s->M; j++)
             if (fr->mask >> j & 1u) O += s->t[j];
-        O /= OR_M;
+        O /= s->M;
         for (int k = 0; k < 3; k++) s->C[k] += s->Te * O * fr->alpha * fr->rgb[k];
-        for (int j = 0; j < OR_M; j++)
+        for (int j = 0; j < s->M; j++)
             if (fr->mask >> j & 1u) s->t[j] *= (1.0 - fr->alpha);
-        s->Teff = s->Te * mean_t(s);
+        s->Tl *= (1.0 - popc_frac(s, fr->mask) * fr->alpha);
+        s->Teff = exit_T(s);
     }
     if (s->Teff < (double)set->t_eps) s->done = 1;
 }
 
 static void pix_finish(or_pix *s, const or_settings *set, double out[4]) {
-    if (s->open) { s->T = s->Te * mean_t(s); s->open = 0; }
+    if (s->open) { s->T = exit_T(s); s->open = 0; }
     for (int k = 0; k < 3; k++) out[k] = s->C[k] + s->T * (double)set->bg_alpha * (double)set->bg[k];
     out[3] = s->T;
 }
@@ -601,7 +685,7 @@ static void pix_finish(or_pix *s, const or_settings *set, double out[4]) {
 /* Blend an explicit fragment list (worked examples, pins). trace[i] = T_eff after fragment i. */
 int or_blend_fragments(const or_frag *fr, int n, const or_settings *set, double out[4], double *trace) {
     or_pix s;
-    pix_init(&s);
+    pix_init(&s, set);
     int used = 0;
     for (int i = 0; i < n && !s.done; i++) {
         pix_apply(&s, fr + i, set);
@@ -617,7 +701,7 @@ static void render_pixel_tiled(const or_ctx *c, int x, int y, double out[4]) {
     int tile = (y / OR_TILE) * c->tiles_x + (x / OR_TILE);
     uint32_t b = c->ranges[2 * tile], e = c->ranges[2 * tile + 1];
     or_pix s;
-    pix_init(&s);
+    pix_init(&s, &c->set);
     or_frag fr;
     for (uint32_t i = b; i < e && !s.done; i++) {
         uint32_t p = c->vals[i];
@@ -720,9 +804,75 @@ int or_render_bruteforce(or_ctx *c, double *out, int nthreads) {
                 int64_t n = or_pixel_fragments(c, x, y, buf, cap);
                 double *o = out + 4 * ((int64_t)y * W + x);
                 or_pix s;
-                pix_init(&s);
+                pix_init(&s, &c->set);
                 for (int64_t i = 0; i < n && !s.done; i++) pix_apply(&s, buf + i, &c->set);
                 pix_finish(&s, &c->set, o);
+            }
+        free(buf);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Supersampled ground truth (used for the Fig.4 overflow / AA
+ * checks, not for parity): each pixel = mean over S x S sub-samples of exact
+ * ordered alpha blending at the sub-sample -- Gaussian alpha evaluated there,
+ * triangle coverage point-wise (same integer edge test) and colour shaded
+ * there; every fragment is a full-coverage alpha blend (Eq.1-2).  Brute force
+ * over all projected primitives, order (depth bits, id).                       */
+int or_render_supersampled(or_ctx *c, double *out, int S, int nthreads) {
+    if (!c->g_rec || S < 1 || 256 % S) return 1;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    const int64_t P = c->F + c->N;
+    const int H = c->cam.height, W = c->cam.width;
+#pragma omp parallel
+    {
+        or_frag *buf = (or_frag *)malloc(sizeof(or_frag) * (P + 1));
+#pragma omp for schedule(dynamic, 1)
+        for (int y = 0; y < H; y++)
+            for (int x = 0; x < W; x++) {
+                double acc[4] = {0, 0, 0, 0};
+                for (int sj = 0; sj < S; sj++)
+                    for (int si = 0; si < S; si++) {
+                        const int64_t PX = 256 * (int64_t)x + (2 * si + 1) * (128 / S);
+                        const int64_t PY = 256 * (int64_t)y + (2 * sj + 1) * (128 / S);
+                        const double px = PX / 256.0, py = PY / 256.0;
+                        int64_t n = 0;
+                        for (int64_t f = 0; f < c->F; f++) {
+                            if (!c->t_touched[f] || !or_inside(c->t_xy + 6 * f, PX, PY)) continue;
+                            buf[n].id = (uint32_t)f; buf[n].kind = 1; buf[n].mask = 1; buf[n].depth = c->t_depth[f];
+                            buf[n].alpha = (double)c->topac[f];
+                            triangle_colour_at(c, f, PX, PY, buf[n].rgb);
+                            n++;
+                        }
+                        for (int64_t g = 0; g < c->N; g++) {
+                            if (!c->g_touched[g]) continue;
+                            const float *rec = c->g_rec + 8 * g;
+                            const double dx = px - rec[0], dy = py - rec[1];
+                            const double q = rec[4] * dx * dx + 2.0 * rec[5] * dx * dy + rec[6] * dy * dy;
+                            if (!(q <= rec[2])) continue;
+                            double a = (double)rec[3] * exp(-0.5 * q);
+                            if (a > (double)c->set.alpha_max) a = (double)c->set.alpha_max;
+                            buf[n].id = (uint32_t)(g + c->F); buf[n].kind = 0; buf[n].mask = 0; buf[n].depth = rec[7];
+                            buf[n].alpha = a;
+                            for (int k = 0; k < 3; k++) buf[n].rgb[k] = c->g_rgb[3 * g + k];
+                            n++;
+                        }
+                        qsort(buf, (size_t)n, sizeof(or_frag), frag_cmp);
+                        double T = 1.0, C[3] = {0, 0, 0};
+                        for (int64_t i = 0; i < n; i++) {
+                            for (int k = 0; k < 3; k++) C[k] += T * buf[i].alpha * buf[i].rgb[k];
+                            T *= 1.0 - buf[i].alpha;
+                        }
+                        for (int k = 0; k < 3; k++) acc[k] += C[k] + T * (double)c->set.bg_alpha * (double)c->set.bg[k];
+                        acc[3] += T;
+                    }
+                double *o = out + 4 * ((int64_t)y * W + x);
+                for (int k = 0; k < 4; k++) o[k] = acc[k] / ((double)S * S);
             }
         free(buf);
     }
