@@ -106,20 +106,28 @@ typedef struct {
     int32_t tex_width, tex_height;
 } unimgs_mesh;
 
-/* Render settings.  Only msaa_samples = 4, tile_size = 16
- * and alpha_min = 1/255 are supported (else UNIMGS_ERR_UNSUPPORTED).
+/* Render settings.  msaa_samples M in {1, 2, 4, 8, 16} (Direct3D
+ * standard patterns; the paper uses 4); tile_size = 16 and alpha_min =
+ * 1/255 only (else UNIMGS_ERR_UNSUPPORTED).
  * alpha_max clamps Gaussian alpha; t_eps is the blend-then-test
  * termination threshold (R16); dilation is added to the cov2d diagonal
  * (S:194); out = C + T * bg_alpha * bg (Eq.10 under reading R5).
  * sort_mode: 0 = factored sort (32-bit depth sort of the visible primitives,
  * then a stable 2-pass radix sort of the pairs by tile), 1 = one onesweep over
- * 64-bit (tile << 32 | depth) keys.  Both produce the identical order. */
+ * 64-bit (tile << 32 | depth) keys.  Both produce the identical order.
+ * blend_mode (the paper's ablation, Fig.3 / Fig.4):
+ *   0 = exact depth-adjacent entity (the method; exit T = T_e * mean_j t_j, R3)
+ *   1 = naive: triangle fragments blended at full coverage (Fig.3a / 4a)
+ *   2 = per-pixel MSAA with alpha, geometric coverage (Eq.5-6)
+ *   3 = whole-pixel entity across Gaussians (Fig.3b-c / 4c, colour overflow)
+ *   4 = exact entity with the paper-literal exit update T *= (1 - O_geo alpha)
+ *       per triangle (Eq.6 as "still updated by Eq.(6)")            */
 typedef struct {
     int32_t msaa_samples, tile_size;
     float alpha_min, alpha_max, t_eps, dilation;
     float bg[3], bg_alpha;
     int32_t sort_mode;
-    int32_t reserved_;
+    int32_t blend_mode;
 } unimgs_settings;
 
 typedef struct {

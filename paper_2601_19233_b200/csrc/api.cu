@@ -76,7 +76,11 @@ extern "C" void unimgs_default_settings(unimgs_settings *s) {
 }
 
 static int validate_settings(unimgs_ctx *c, const unimgs_settings *s) {
-    if (s->msaa_samples != 4) return fail(c, UNIMGS_ERR_UNSUPPORTED, "msaa_samples must be 4 (got %d)", s->msaa_samples);
+    if (s->msaa_samples != 1 && s->msaa_samples != 2 && s->msaa_samples != 4 && s->msaa_samples != 8 &&
+        s->msaa_samples != 16)
+        return fail(c, UNIMGS_ERR_UNSUPPORTED, "msaa_samples must be 1, 2, 4, 8 or 16 (got %d)", s->msaa_samples);
+    if (s->blend_mode < 0 || s->blend_mode > 4)
+        return fail(c, UNIMGS_ERR_UNSUPPORTED, "blend_mode must be 0..4 (got %d)", s->blend_mode);
     if (s->tile_size != 16) return fail(c, UNIMGS_ERR_UNSUPPORTED, "tile_size must be 16 (got %d)", s->tile_size);
     if (!(fabs((double)s->alpha_min - 1.0 / 255.0) < 1e-9))
         return fail(c, UNIMGS_ERR_UNSUPPORTED, "alpha_min must be 1/255 (got %g)", (double)s->alpha_min);
@@ -271,7 +275,8 @@ extern "C" int unimgs_render(unimgs_ctx *c, float *out, void *stream) {
     if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
     if (c->stage < 2) return fail(c, UNIMGS_ERR_STATE, "render before bin");
     if (!out) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "out is NULL");
-    BlendParams bp{c->set.alpha_max, c->set.t_eps, c->set.bg_alpha, {c->set.bg[0], c->set.bg[1], c->set.bg[2]}};
+    BlendParams bp{c->set.alpha_max, c->set.t_eps, c->set.bg_alpha, {c->set.bg[0], c->set.bg[1], c->set.bg[2]},
+                   c->set.blend_mode, c->set.msaa_samples};
     c->launches += launch_blend(c->buf, c->g, c->m, c->cam, bp, out, (cudaStream_t)stream);
     return check_launch(c, "render");
 }
@@ -282,7 +287,8 @@ extern "C" int unimgs_render_counted(unimgs_ctx *c, float *out, int64_t *work_ho
     if (!out || !work_host) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "out/work is NULL");
     cudaStream_t s = (cudaStream_t)stream;
     CUDA_TRY(c, cudaMemsetAsync(c->buf.st->work, 0, sizeof(c->buf.st->work), s));
-    BlendParams bp{c->set.alpha_max, c->set.t_eps, c->set.bg_alpha, {c->set.bg[0], c->set.bg[1], c->set.bg[2]}};
+    BlendParams bp{c->set.alpha_max, c->set.t_eps, c->set.bg_alpha, {c->set.bg[0], c->set.bg[1], c->set.bg[2]},
+                   c->set.blend_mode, c->set.msaa_samples};
     c->launches += launch_blend(c->buf, c->g, c->m, c->cam, bp, out, s, true);
     int rc = check_launch(c, "render_counted");
     if (rc) return rc;

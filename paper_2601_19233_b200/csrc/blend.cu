@@ -11,8 +11,8 @@
 //   Gaussian fragment  iff q <= q_max (N6, bit-exact with the oracle):
 //       close an open entity (T = T_e * mean_j t_j, reading R3),
 //       alpha = min(alpha_max, o e^{-q/2}); C += T alpha c; T *= 1 - alpha  (Eq.1-2)
-//   triangle fragment  iff its 4-sample coverage mask m != 0 (exact int64
-//       edge functions, top-left rule, D3D 4x pattern; N7, R10-R11):
+//   triangle fragment  iff its M-sample coverage mask m != 0 (exact int64
+//       edge functions, top-left rule, D3D patterns, M = 4 by default; N7, R10-R11):
 //       open an entity if none (T_e = T, t_j = 1; Eq.7), O = sum_j m_j t_j / 4
 //       (Eq.8), C += T_e O alpha c (Eq.9), t_j *= 1 - m_j alpha (Eq.7)
 //   stop once T_eff < t_eps (blend-then-test, R16); a warp exits when all of
@@ -40,25 +40,51 @@ __device__ __forceinline__ float4 texel(const TexView &t, int i, int j) {
     return make_float4(c.x, c.y, c.z, c.w);
 }
 
-// 4x coverage mask of a triangle record at pixel (x, y): sample j at
-// (256x + 128 + 16 ox_j, 256y + 128 + 16 oy_j), offsets (-2,-6) (6,-2) (-6,2) (2,6).
+// Direct3D standard multisample patterns, 1/16 px from the pixel centre (R10);
+// M = 4 is the paper's setting.
+template <int M>
+__device__ __forceinline__ void sample_offset(int j, int &ox, int &oy) {
+    if (M == 1) { ox = 0; oy = 0; return; }
+    if (M == 2) {
+        constexpr int P[2][2] = {{4, 4}, {-4, -4}};
+        ox = P[j][0]; oy = P[j][1]; return;
+    }
+    if (M == 4) {
+        constexpr int P[4][2] = {{-2, -6}, {6, -2}, {-6, 2}, {2, 6}};
+        ox = P[j][0]; oy = P[j][1]; return;
+    }
+    if (M == 8) {
+        constexpr int P[8][2] = {{1, -3}, {-1, 3}, {5, 1}, {-3, -5}, {-5, 5}, {-7, -1}, {3, 7}, {7, -7}};
+        ox = P[j][0]; oy = P[j][1]; return;
+    }
+    constexpr int P[16][2] = {{1, 1}, {-1, -3}, {-3, 2}, {4, -1}, {-5, -2}, {2, 5}, {5, 3}, {3, -5},
+                              {-2, 6}, {0, -7}, {-4, -6}, {-6, 4}, {-8, 0}, {7, -4}, {6, 7}, {-7, -8}};
+    ox = P[j][0]; oy = P[j][1];
+}
+
+// M-sample coverage mask of a triangle record at pixel (x, y): sample j at
+// (256x + 128 + 16 ox_j, 256y + 128 + 16 oy_j) in 1/256 px; exact int64 edge
+// functions with the top-left-style rule (N7, R11).  Ec = edge functions at the centre.
+template <int M>
 __device__ __forceinline__ unsigned coverage(const int X[3], const int Y[3], int x, int y, long long Ec[3]) {
     const int PX = 256 * x + 128, PY = 256 * y + 128;
-    unsigned m = 0xF;
+    unsigned m = (M == 32) ? 0xFFFFFFFFu : ((1u << M) - 1u);
 #pragma unroll
     for (int k = 0; k < 3; k++) {
         const int a = (k + 1) % 3, b = (k + 2) % 3;
         const int dx = X[b] - X[a], dy = Y[b] - Y[a];
-        // E_k(P) = dx (PY - Ya) - dy (PX - Xa) at the centre, then per-sample offsets
+        // E_k(P) = dx (PY - Ya) - dy (PX - Xa) at the centre, then per-sample offsets 16 (dx oy - dy ox)
         const long long e = (long long)dx * (PY - Y[a]) - (long long)dy * (PX - X[a]);
         Ec[k] = e;
         const long long thr = (dy > 0 || (dy == 0 && dx < 0)) ? 0 : 1;
-        // sample offsets (in 1/256 px): 16 * (dx * oy - dy * ox)
-        const long long e0 = e + 16LL * ((long long)dx * -6 - (long long)dy * -2);
-        const long long e1 = e + 16LL * ((long long)dx * -2 - (long long)dy * 6);
-        const long long e2 = e + 16LL * ((long long)dx * 2 - (long long)dy * -6);
-        const long long e3 = e + 16LL * ((long long)dx * 6 - (long long)dy * 2);
-        unsigned mk = (e0 >= thr ? 1u : 0u) | (e1 >= thr ? 2u : 0u) | (e2 >= thr ? 4u : 0u) | (e3 >= thr ? 8u : 0u);
+        unsigned mk = 0;
+#pragma unroll
+        for (int j = 0; j < M; j++) {
+            int ox, oy;
+            sample_offset<M>(j, ox, oy);
+            const long long ej = e + 16LL * ((long long)dx * oy - (long long)dy * ox);
+            mk |= (ej >= thr ? 1u : 0u) << j;
+        }
         m &= mk;
     }
     return m;
@@ -137,45 +163,78 @@ __device__ __forceinline__ float ex2_ftz(float x) {
     return y;
 }
 
-// Per-pixel blend state (registers).
+// blend modes (the paper's ablation, Fig.3 / Fig.4)
+enum { MODE_EXACT = 0, MODE_NAIVE = 1, MODE_MSAA_PIXEL = 2, MODE_WHOLE_PIXEL = 3, MODE_PAPER_LITERAL = 4 };
+
+// Per-pixel blend state (registers).  G / Tl only exist for the modes that use them.
+template <int MODE, int M>
 struct Px {
-    float C0, C1, C2, T, Te, t0, t1, t2, t3;
+    float C0, C1, C2, T, Te;
+    float t[M];
+    float G, Tl;
     bool open, done;
+    __device__ __forceinline__ float mean_t() const {
+        float a = 0.f;
+#pragma unroll
+        for (int j = 0; j < M; j++) a += t[j];
+        return a * (1.f / M);
+    }
+    // transmittance leaving the entity (R3; Eq.6 product for the paper-literal mode)
+    __device__ __forceinline__ float exit_T() const {
+        if (MODE == MODE_PAPER_LITERAL) return Tl;
+        if (MODE == MODE_WHOLE_PIXEL) return Te * mean_t() * G;
+        return Te * mean_t();
+    }
 };
 
-// One triangle fragment candidate at pixel (x, y): coverage, then Eq.7-9.
-template <bool COUNT>
-#ifdef UNIMGS_TRI_NOINLINE
-__device__ __noinline__
-#else
-__device__ __forceinline__
-#endif
-void tri_pixel(Px &s, const TriRecord &r, int x, int y, const TexView &tv, float t_eps,
-                                          unsigned long long &w_tt, unsigned long long &w_tf) {
+template <int M>
+__device__ __forceinline__ float popc_frac(unsigned m) {
+    return (float)__popc(m) * (1.f / M);
+}
+
+// One triangle fragment candidate at pixel (x, y): coverage, then the mode's update
+// (exact: Eq.7-9 in a depth-adjacent entity).
+template <bool COUNT, int MODE, int M>
+__device__ __forceinline__ void tri_pixel(Px<MODE, M> &s, const TriRecord &r, int x, int y, const TexView &tv,
+                                          float t_eps, unsigned long long &w_tt, unsigned long long &w_tf) {
     const int4 q0 = r.q0, q1 = r.q1;
     const int X[3] = {q0.x, q0.z, q1.x}, Y[3] = {q0.y, q0.w, q1.y};
     long long Ec[3];
     if (COUNT) w_tt++;
-    const unsigned m = coverage(X, Y, x, y, Ec);
+    const unsigned m = coverage<M>(X, Y, x, y, Ec);
     if (!m) return;
     if (COUNT) w_tf++;
     float rgb[3];
     tri_colour(r, Ec, tv, rgb);
     const float al = __int_as_float(q1.w);
+    if (MODE == MODE_NAIVE || MODE == MODE_MSAA_PIXEL) {
+        const float O = MODE == MODE_NAIVE ? 1.f : popc_frac<M>(m);  // full / geometric coverage (Eq.5-6)
+        const float w = s.T * O * al;
+        s.C0 += w * rgb[0]; s.C1 += w * rgb[1]; s.C2 += w * rgb[2];
+        s.T -= w;
+        if (s.T < t_eps) s.done = true;
+        return;
+    }
     if (!s.open) {
         s.open = true;
         s.Te = s.T;
-        s.t0 = s.t1 = s.t2 = s.t3 = 1.f;
+        s.G = 1.f;
+        s.Tl = s.T;
+#pragma unroll
+        for (int j = 0; j < M; j++) s.t[j] = 1.f;
     }
-    const float O = (((m & 1) ? s.t0 : 0.f) + ((m & 2) ? s.t1 : 0.f) + ((m & 4) ? s.t2 : 0.f) + ((m & 8) ? s.t3 : 0.f)) * 0.25f;
-    const float w = s.Te * O * al;
+    float O = 0.f;
+#pragma unroll
+    for (int j = 0; j < M; j++) O += ((m >> j) & 1u) ? s.t[j] : 0.f;
+    O *= 1.f / M;  // Eq.8
+    const float w = s.Te * O * al;  // Eq.9
     s.C0 += w * rgb[0]; s.C1 += w * rgb[1]; s.C2 += w * rgb[2];
     const float kk = 1.f - al;
-    if (m & 1) s.t0 *= kk;
-    if (m & 2) s.t1 *= kk;
-    if (m & 4) s.t2 *= kk;
-    if (m & 8) s.t3 *= kk;
-    if (s.Te * ((s.t0 + s.t1) + (s.t2 + s.t3)) * 0.25f < t_eps) s.done = true;
+#pragma unroll
+    for (int j = 0; j < M; j++)
+        if ((m >> j) & 1u) s.t[j] *= kk;  // Eq.7
+    if (MODE == MODE_PAPER_LITERAL) s.Tl *= 1.f - popc_frac<M>(m) * al;
+    if (s.exit_T() < t_eps) s.done = true;
 }
 
 // One CTA per 16x16 tile, independent warps, PIX pixels per lane (vertically
@@ -190,7 +249,7 @@ void tri_pixel(Px &s, const TriRecord &r, int x, int y, const TexView &tv, float
 #ifndef UNIMGS_BLEND_MINB
 #define UNIMGS_BLEND_MINB (4 * PIX)
 #endif
-template <bool COUNT, int PIX>
+template <bool COUNT, int PIX, int MODE, int M>
 __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blend(const uint2 *__restrict__ ranges,
                                                                      const uint32_t *__restrict__ vals,
                                                                      const GaussRecord *__restrict__ grec,
@@ -215,12 +274,13 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
     const unsigned lt = (1u << lane) - 1u;
     float4(*buf)[3] = s_buf[warp];
 
-    Px s[PIX];
+    Px<MODE, M> s[PIX];
 #pragma unroll
     for (int p = 0; p < PIX; p++) {
         s[p].C0 = s[p].C1 = s[p].C2 = 0.f;
-        s[p].T = s[p].Te = 1.f;
-        s[p].t0 = s[p].t1 = s[p].t2 = s[p].t3 = 1.f;
+        s[p].T = s[p].Te = s[p].G = s[p].Tl = 1.f;
+#pragma unroll
+        for (int j = 0; j < M; j++) s[p].t[j] = 1.f;
         s[p].open = false;
         s[p].done = !(x < W && y0 + 4 * p < H);
     }
@@ -296,8 +356,18 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
                 if (!hit[p]) continue;
                 if (COUNT) w_gf++;
                 const float al = fminf(bp.alpha_max, ea.w * ex2_ftz(q[p] * kexp));
-                if (s[p].open) {
-                    s[p].T = s[p].Te * ((s[p].t0 + s[p].t1) + (s[p].t2 + s[p].t3)) * 0.25f;
+                if (MODE == MODE_WHOLE_PIXEL && s[p].open) {
+                    // Fig.3b/c: the entity spans the whole list; the Gaussian does not
+                    // attenuate its sub-pixel state (colour overflow)
+                    const float base = s[p].Te * s[p].mean_t();
+                    const float w = base * s[p].G * al;
+                    s[p].C0 += w * ec.x; s[p].C1 += w * ec.y; s[p].C2 += w * ec.z;
+                    s[p].G *= 1.f - al;
+                    if (base * s[p].G < bp.t_eps) s[p].done = true;
+                    continue;
+                }
+                if (MODE != MODE_NAIVE && MODE != MODE_MSAA_PIXEL && s[p].open) {
+                    s[p].T = s[p].exit_T();  // depth adjacency broken
                     s[p].open = false;
                 }
                 const float w = s[p].T * al;
@@ -325,7 +395,7 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
                     const TriRecord &r = trec[__float_as_uint(eb.w)];
 #pragma unroll
                     for (int p = 0; p < PIX; p++)
-                        if (!s[p].done) tri_pixel<COUNT>(s[p], r, x, y0 + 4 * p, tv, bp.t_eps, w_tt, w_tf);
+                        if (!s[p].done) tri_pixel<COUNT, MODE, M>(s[p], r, x, y0 + 4 * p, tv, bp.t_eps, w_tt, w_tf);
                 }
             }
         }
@@ -346,27 +416,51 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
         const int y = y0 + 4 * p;
         if (x < W && y < H) {
             float T = s[p].T;
-            if (s[p].open) T = s[p].Te * ((s[p].t0 + s[p].t1) + (s[p].t2 + s[p].t3)) * 0.25f;
+            if (s[p].open) T = s[p].exit_T();
             const float sb = T * bp.bg_alpha;
             out[(size_t)y * W + x] = make_float4(s[p].C0 + sb * bp.bg[0], s[p].C1 + sb * bp.bg[1], s[p].C2 + sb * bp.bg[2], T);
         }
     }
 }
 
-int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, const CamParams &cam,
-                 const BlendParams &bp, float *out, cudaStream_t s, bool count_work) {
-    (void)g;
+template <int MODE, int M>
+static void launch_mode(const Buffers &b, const MeshInput &m, const CamParams &cam, const BlendParams &bp, float *out,
+                        cudaStream_t s, bool count_work) {
     constexpr int PIX = UNIMGS_BLEND_PIX;
     const int tiles = cam.tiles_x * cam.tiles_y;
     TexView tv{reinterpret_cast<const uchar4 *>(m.tex), m.tw, m.th};
     if (count_work)
-        k_blend<true, PIX><<<tiles, kBlendThreads / PIX, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv,
-                                                                 (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
-                                                                 reinterpret_cast<float4 *>(out), b.st);
+        k_blend<true, PIX, MODE, M><<<tiles, kBlendThreads / PIX, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv,
+                                                                        (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
+                                                                        reinterpret_cast<float4 *>(out), b.st);
     else
-        k_blend<false, PIX><<<tiles, kBlendThreads / PIX, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv,
-                                                                  (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
-                                                                  reinterpret_cast<float4 *>(out), b.st);
+        k_blend<false, PIX, MODE, M><<<tiles, kBlendThreads / PIX, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv,
+                                                                         (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
+                                                                         reinterpret_cast<float4 *>(out), b.st);
+}
+
+template <int MODE>
+static void launch_m(int M, const Buffers &b, const MeshInput &m, const CamParams &cam, const BlendParams &bp,
+                     float *out, cudaStream_t s, bool count_work) {
+    switch (M) {
+        case 1: launch_mode<MODE, 1>(b, m, cam, bp, out, s, count_work); break;
+        case 2: launch_mode<MODE, 2>(b, m, cam, bp, out, s, count_work); break;
+        case 8: launch_mode<MODE, 8>(b, m, cam, bp, out, s, count_work); break;
+        case 16: launch_mode<MODE, 16>(b, m, cam, bp, out, s, count_work); break;
+        default: launch_mode<MODE, 4>(b, m, cam, bp, out, s, count_work); break;
+    }
+}
+
+int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, const CamParams &cam,
+                 const BlendParams &bp, float *out, cudaStream_t s, bool count_work) {
+    (void)g;
+    switch (bp.mode) {
+        case MODE_NAIVE: launch_m<MODE_NAIVE>(bp.msaa, b, m, cam, bp, out, s, count_work); break;
+        case MODE_MSAA_PIXEL: launch_m<MODE_MSAA_PIXEL>(bp.msaa, b, m, cam, bp, out, s, count_work); break;
+        case MODE_WHOLE_PIXEL: launch_m<MODE_WHOLE_PIXEL>(bp.msaa, b, m, cam, bp, out, s, count_work); break;
+        case MODE_PAPER_LITERAL: launch_m<MODE_PAPER_LITERAL>(bp.msaa, b, m, cam, bp, out, s, count_work); break;
+        default: launch_m<MODE_EXACT>(bp.msaa, b, m, cam, bp, out, s, count_work); break;
+    }
     return 1;
 }
 

@@ -96,6 +96,8 @@ struct MeshInput {
 struct BlendParams {
     float alpha_max, t_eps, bg_alpha;
     float bg[3];
+    int mode;   // unimgs_settings::blend_mode
+    int msaa;   // M samples
 };
 
 // ---- launchers (return number of kernels enqueued) --------------------------
