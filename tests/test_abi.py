@@ -59,6 +59,6 @@ def test_no_device_calls_fail_cleanly_without_gpu():
     s = _lib.Settings()
     L.unimgs_default_settings(ctypes.byref(s))
     assert s.msaa_samples == 4 and s.tile_size == 16 and abs(s.alpha_max - 0.99) < 1e-7
-    s.msaa_samples = 8
+    s.msaa_samples = 3  # only 1, 2, 4, 8, 16
     h = ctypes.c_void_p()
     assert L.unimgs_create(ctypes.byref(h), ctypes.byref(s)) == _lib.ERR_UNSUPPORTED
