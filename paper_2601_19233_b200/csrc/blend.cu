@@ -172,6 +172,7 @@ struct Px {
     float C0, C1, C2, T, Te;
     float t[M];
     float G, Tl;
+    float Tx;  // cached exit transmittance of the open entity (refreshed by each triangle)
     bool open, done;
     __device__ __forceinline__ float mean_t() const {
         float a = 0.f;
@@ -234,7 +235,8 @@ __device__ __forceinline__ void tri_pixel(Px<MODE, M> &s, const TriRecord &r, in
     for (int j = 0; j < M; j++)
         if ((m >> j) & 1u) s.t[j] *= kk;  // Eq.7
     if (MODE == MODE_PAPER_LITERAL) s.Tl *= 1.f - popc_frac<M>(m) * al;
-    if (s.exit_T() < t_eps) s.done = true;
+    s.Tx = s.exit_T();
+    if (s.Tx < t_eps) s.done = true;
 }
 
 // One CTA per 16x16 tile, independent warps, PIX pixels per lane (vertically
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
 #pragma unroll
     for (int p = 0; p < PIX; p++) {
         s[p].C0 = s[p].C1 = s[p].C2 = 0.f;
-        s[p].T = s[p].Te = s[p].G = s[p].Tl = 1.f;
+        s[p].T = s[p].Te = s[p].G = s[p].Tl = s[p].Tx = 1.f;
 #pragma unroll
         for (int j = 0; j < M; j++) s[p].t[j] = 1.f;
         s[p].open = false;
@@ -367,7 +369,7 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
                     continue;
                 }
                 if (MODE != MODE_NAIVE && MODE != MODE_MSAA_PIXEL && s[p].open) {
-                    s[p].T = s[p].exit_T();  // depth adjacency broken
+                    s[p].T = s[p].Tx;  // depth adjacency broken: exit T (R3)
                     s[p].open = false;
                 }
                 const float w = s[p].T * al;
