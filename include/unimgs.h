@@ -85,12 +85,35 @@ typedef struct {
 /* 3D Gaussians (3DGS parameterisation).  means [N][3], quats [N][4]
  * (w, x, y, z; need not be normalised), scales [N][3] linear, opacities [N]
  * post-sigmoid in [0, 1], sh [N][(D+1)^2][3] real SH in the 3DGS basis,
- * D = sh_degree in 0..3.  count may be 0 (then pointers may be NULL). */
+ * D = sh_degree in 0..3.  cov3d [N][6] (xx xy xz yy yz zz), optional: when
+ * non-NULL it is Sigma and quats/scales are ignored (may be NULL) -- e.g. the
+ * output of unimgs_deform.  count may be 0 (then pointers may be NULL). */
 typedef struct {
     int64_t count;
     const float *means, *quats, *scales, *opacities, *sh;
     int32_t sh_degree;
+    const float *cov3d;
 } unimgs_gaussians;
+
+/* Gaussian-to-mesh binding: K = 1 (ray through the centre,
+ * "UniMGS*") or 8 (rays to the BBX corners) anchors per Gaussian; face [N][K]
+ * (< 0 = unbound anchor), bary [N][K][3] barycentric (u, v, w) of the anchor. */
+typedef struct {
+    int64_t count;
+    int32_t anchors;
+    const int32_t *face;
+    const float *bary;
+} unimgs_binding;
+
+/* Per-vertex transforms of the manipulated proxy mesh (from ACAP or
+ * any mesh deformer): delta [V][3] = V' - V, log_rot [V][3] the rotation as an
+ * axis-angle vector, shear [V][6] the symmetric shear S (xx xy xz yy yz zz);
+ * faces [F][3] of the rest mesh. */
+typedef struct {
+    int64_t num_vertices, num_faces;
+    const int32_t *faces;
+    const float *delta, *log_rot, *shear;
+} unimgs_vertex_field;
 
 /* Triangle mesh with a per-triangle opacity (reading R13).
  * positions [V][3]; faces [F][3] int32 vertex ids; opacity [F] in [0, 1].
@@ -175,6 +198,15 @@ UNIMGS_API int unimgs_bin(unimgs_ctx *c, void *stream);
  * out_rgbt [height][width][4] float32 (R, G, B, final T), device pointer.
  * Must follow unimgs_bin. */
 UNIMGS_API int unimgs_render(unimgs_ctx *c, float *out_rgbt, void *stream);
+
+/* Deformation transfer, Eq.12-13, one thread per Gaussian:
+ * blend (Delta, log R, S) barycentrically at each bound anchor (Eq.12), then
+ * R' = exp(mean log R_i), S' = mean S_i, Sigma' = R'S' Sigma (R'S')^T,
+ * mu' = mu + mean Delta_i (Eq.13).  Sigma from rest->cov3d or quats/scales.
+ * Writes means_out [N][3] and cov_out [N][6] (device; pass them as means and
+ * cov3d of the next unimgs_preprocess).  No context, no allocation, no sync. */
+UNIMGS_API int unimgs_deform(const unimgs_gaussians *rest, const unimgs_binding *binding,
+                             const unimgs_vertex_field *field, float *means_out, float *cov_out, void *stream);
 
 /* Measurement variant of unimgs_render: identical output, plus the blend's
  * work counts (host work[4]): Gaussian entries tested, Gaussian fragments

@@ -95,6 +95,12 @@ def lib():
         L.or_render_supersampled.argtypes = [vp, vp, i32, i32]
         L.or_render_supersampled.restype = i32
         L.or_sh_basis_colour.argtypes = [vp, i32, vp, vp]
+        L.or_set_cov3d.argtypes = [vp, vp]
+        L.or_set_cov3d.restype = None
+        L.or_deform.argtypes = [vp, i32, vp, vp, vp, i64, vp, vp, vp, vp, vp]
+        L.or_deform.restype = i32
+        L.or_rodrigues_public.argtypes = [vp, vp]
+        L.or_rodrigues_public.restype = None
         _lib = L
     return _lib
 
@@ -152,6 +158,26 @@ class Oracle:
                        _ptr(k[7]), _ptr(k[8]), _ptr(k[9]), _ptr(k[10]),
                        0 if tex is None else int(tex.shape[1]), 0 if tex is None else int(tex.shape[0]))
         self.cam = None
+        cov = getattr(g, "cov3d", None)
+        if cov is not None:
+            self._cov = np.ascontiguousarray(cov, np.float32)
+            L.or_set_cov3d(self._h, _ptr(self._cov))
+
+    def deform(self, binding, field, faces):
+        """Eq.12-13: deformed (means [N,3], covariances [N,6] xx xy xz yy yz zz) in float64."""
+        face = np.ascontiguousarray(binding.face, np.int32)
+        bary = np.ascontiguousarray(binding.bary, np.float32)
+        fc = np.ascontiguousarray(faces, np.int32)
+        d = np.ascontiguousarray(field.delta, np.float32)
+        lr = np.ascontiguousarray(field.log_rot, np.float32)
+        sh = np.ascontiguousarray(field.shear, np.float32)
+        mu = np.zeros((self.N, 3), np.float64)
+        cv = np.zeros((self.N, 6), np.float64)
+        K = int(face.shape[1])
+        if lib().or_deform(self._h, K, _ptr(face), _ptr(bary), _ptr(fc), int(fc.shape[0]), _ptr(d), _ptr(lr),
+                           _ptr(sh), _ptr(mu), _ptr(cv)):
+            raise ValueError("anchors per Gaussian must be 1..8")
+        return mu, cv
 
     def __del__(self):
         try:
@@ -271,6 +297,12 @@ def frags(*items) -> np.ndarray:
 def coverage_mask(xy6, x: int, y: int) -> int:
     xy = np.ascontiguousarray(xy6, np.int32)
     return int(lib().or_coverage_mask(_ptr(xy), x, y))
+
+
+def rodrigues(w) -> np.ndarray:
+    R = np.zeros(9, np.float64)
+    lib().or_rodrigues_public(_ptr(np.ascontiguousarray(w, np.float64)), _ptr(R))
+    return R.reshape(3, 3)
 
 
 def coverage_mask_m(xy6, x: int, y: int, M: int) -> int:

@@ -69,6 +69,7 @@ typedef struct {
     /* scene (borrowed pointers) */
     int64_t N, V, F;
     const float *means, *quats, *scales, *opac, *sh;
+    const float *cov3d; /* optional [N][6] xx xy xz yy yz zz: replaces quats/scales (N3) */
     int sh_degree;
     const float *pos, *uvs, *cols, *topac;
     const int32_t *faces;
@@ -126,6 +127,8 @@ void or_set_scene(or_ctx *c, int64_t N, const float *means, const float *quats, 
     c->V = V; c->F = F; c->pos = pos; c->uvs = uvs; c->cols = cols; c->faces = faces; c->topac = topac;
     c->tex = tex; c->tw = tw; c->th = th;
 }
+
+void or_set_cov3d(or_ctx *c, const float *cov3d) { c->cov3d = cov3d; }
 
 /* ------------------------------------------------------------------------- */
 /* N1 view transform: pv[r] = fma(R[r][0],x, fma(R[r][1],y, fma(R[r][2],z, t[r])))          */
@@ -192,6 +195,12 @@ static void project_gaussian(or_ctx *c, int64_t i) {
     float xz = pv[0] / pv[2], yz = pv[1] / pv[2];                               /* N2 */
     float u = fmaf(cam->fx, xz, cam->cx), v = fmaf(cam->fy, yz, cam->cy);
 
+    float Sig[3][3];
+    if (c->cov3d) { /* given covariance (e.g. deformed by Eq.13) */
+        const float *cv = c->cov3d + 6 * i;
+        Sig[0][0] = cv[0]; Sig[0][1] = Sig[1][0] = cv[1]; Sig[0][2] = Sig[2][0] = cv[2];
+        Sig[1][1] = cv[3]; Sig[1][2] = Sig[2][1] = cv[4]; Sig[2][2] = cv[5];
+    } else {
     /* N3: quaternion (w,x,y,z) -> R, Sigma = R S^2 R^T */
     const float *q = c->quats + 4 * i;
     const float *s = c->scales + 3 * i;
@@ -208,9 +217,9 @@ static void project_gaussian(or_ctx *c, int64_t i) {
     float m[3][3];
     for (int a = 0; a < 3; a++)
         for (int b = 0; b < 3; b++) m[a][b] = r[a][b] * s[b];
-    float Sig[3][3];
     for (int a = 0; a < 3; a++)
         for (int b = 0; b < 3; b++) Sig[a][b] = dot3(m[a], m[b]);
+    }
     /* A = W Sigma, Sigma_v = A W^T, W = R_w2c */
     float W[3][3], A[3][3], Sv[3][3];
     for (int a = 0; a < 3; a++)
@@ -875,6 +884,111 @@ int or_render_supersampled(or_ctx *c, double *out, int S, int nthreads) {
                 for (int k = 0; k < 4; k++) o[k] = acc[k] / ((double)S * S);
             }
         free(buf);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Deformation transfer, Eq.12-13, double precision.
+ * Per Gaussian and bound anchor i (K = 1 centre ray or 8 BBX corners)
+ * on face (v1, v2, v3) with barycentrics (u, v, w):
+ *   Delta_i = u Delta^1 + v Delta^2 + w Delta^3,  R_i = u log R^1 + v log R^2 + w log R^3,
+ *   S_i = u S^1 + v S^2 + w S^3                                            (Eq.12)
+ *   R' = exp(mean_i R_i), S' = mean_i S_i, Sigma' = R'S' Sigma (R'S')^T,
+ *   mu' = mu + mean_i Delta_i                                             (Eq.13)
+ * log R is an axis-angle vector (so(3)); exp by Rodrigues' formula.  Anchors with
+ * face < 0 are unbound and skipped (the means are over the bound anchors; a
+ * Gaussian with none keeps mu and Sigma).  Sigma comes from quats/scales
+ * (Sigma = R S^2 R^T) or from cov3d when the scene has one.                 */
+static void or_rodrigues(const double w[3], double R[3][3]) {
+    const double th = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+    double K[3][3] = {{0, -w[2], w[1]}, {w[2], 0, -w[0]}, {-w[1], w[0], 0}};
+    double a, b; /* R = I + a K + b K^2 with a = sin th / th, b = (1 - cos th) / th^2 */
+    if (th < 1e-6) { a = 1.0 - th * th / 6.0; b = 0.5 - th * th / 24.0; }
+    else { a = sin(th) / th; b = (1.0 - cos(th)) / (th * th); }
+    for (int r = 0; r < 3; r++)
+        for (int c2 = 0; c2 < 3; c2++) {
+            double k2 = 0.0;
+            for (int m = 0; m < 3; m++) k2 += K[r][m] * K[m][c2];
+            R[r][c2] = (r == c2 ? 1.0 : 0.0) + a * K[r][c2] + b * k2;
+        }
+}
+
+void or_rodrigues_public(const double *w, double *R) { or_rodrigues(w, (double(*)[3])R); }
+
+int or_deform(const or_ctx *c, int K, const int32_t *face, const float *bary, const int32_t *faces, int64_t F,
+              const float *delta, const float *log_rot, const float *shear, double *mu_out, double *cov_out) {
+    if (K < 1 || K > 8) return 1;
+#pragma omp parallel for schedule(static)
+    for (int64_t g = 0; g < c->N; g++) {
+        double Sig[3][3];
+        if (c->cov3d) {
+            const float *cv = c->cov3d + 6 * g;
+            Sig[0][0] = cv[0]; Sig[0][1] = Sig[1][0] = cv[1]; Sig[0][2] = Sig[2][0] = cv[2];
+            Sig[1][1] = cv[3]; Sig[1][2] = Sig[2][1] = cv[4]; Sig[2][2] = cv[5];
+        } else {
+            const float *q = c->quats + 4 * g, *sc = c->scales + 3 * g;
+            double w = q[0], x = q[1], y = q[2], z = q[3];
+            const double n = sqrt(w * w + x * x + y * y + z * z);
+            w /= n; x /= n; y /= n; z /= n;
+            const double Rg[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+                                     {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
+                                     {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
+            for (int a = 0; a < 3; a++)
+                for (int b = 0; b < 3; b++) {
+                    double acc = 0.0;
+                    for (int m = 0; m < 3; m++) acc += Rg[a][m] * (double)sc[m] * (double)sc[m] * Rg[b][m];
+                    Sig[a][b] = acc;
+                }
+        }
+        double sd[3] = {0, 0, 0}, sl[3] = {0, 0, 0}, ss[6] = {0, 0, 0, 0, 0, 0};
+        int n = 0;
+        for (int i = 0; i < K; i++) {
+            const int32_t f = face[g * K + i];
+            if (f < 0 || f >= F) continue;
+            const float *bw = bary + 3 * (g * K + i);
+            for (int j = 0; j < 3; j++) {
+                const int64_t v = faces[3 * (int64_t)f + j];
+                const double wj = bw[j];
+                for (int a = 0; a < 3; a++) {
+                    sd[a] += wj * delta[3 * v + a];
+                    sl[a] += wj * log_rot[3 * v + a];
+                }
+                for (int a = 0; a < 6; a++) ss[a] += wj * shear[6 * v + a];
+            }
+            n++;
+        }
+        double *mo = mu_out + 3 * g, *co = cov_out + 6 * g;
+        if (n == 0) {
+            for (int a = 0; a < 3; a++) mo[a] = c->means[3 * g + a];
+            co[0] = Sig[0][0]; co[1] = Sig[0][1]; co[2] = Sig[0][2]; co[3] = Sig[1][1]; co[4] = Sig[1][2]; co[5] = Sig[2][2];
+            continue;
+        }
+        double Rm[3][3], L[3] = {sl[0] / n, sl[1] / n, sl[2] / n};
+        or_rodrigues(L, Rm);
+        const double S[3][3] = {{ss[0] / n, ss[1] / n, ss[2] / n}, {ss[1] / n, ss[3] / n, ss[4] / n},
+                                {ss[2] / n, ss[4] / n, ss[5] / n}};
+        double A[3][3], AS[3][3], Sp[3][3];
+        for (int a = 0; a < 3; a++)
+            for (int b = 0; b < 3; b++) {
+                double acc = 0.0;
+                for (int m = 0; m < 3; m++) acc += Rm[a][m] * S[m][b];
+                A[a][b] = acc;
+            }
+        for (int a = 0; a < 3; a++)
+            for (int b = 0; b < 3; b++) {
+                double acc = 0.0;
+                for (int m = 0; m < 3; m++) acc += A[a][m] * Sig[m][b];
+                AS[a][b] = acc;
+            }
+        for (int a = 0; a < 3; a++)
+            for (int b = 0; b < 3; b++) {
+                double acc = 0.0;
+                for (int m = 0; m < 3; m++) acc += AS[a][m] * A[b][m];
+                Sp[a][b] = acc;
+            }
+        for (int a = 0; a < 3; a++) mo[a] = (double)c->means[3 * g + a] + sd[a] / n;
+        co[0] = Sp[0][0]; co[1] = Sp[0][1]; co[2] = Sp[0][2]; co[3] = Sp[1][1]; co[4] = Sp[1][2]; co[5] = Sp[2][2];
     }
     return 0;
 }

@@ -18,7 +18,7 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "UNSUPPORTED", 3: "CAPACITY",
 EXPORTS = ("unimgs_default_settings", "unimgs_create", "unimgs_set_settings", "unimgs_reserve", "unimgs_reserve2",
            "unimgs_preprocess", "unimgs_bin", "unimgs_render", "unimgs_render_counted", "unimgs_get_stats", "unimgs_get_bins",
            "unimgs_get_records", "unimgs_render_host", "unimgs_launch_count", "unimgs_error_string",
-           "unimgs_destroy")
+           "unimgs_destroy", "unimgs_deform")
 
 
 class Camera(C.Structure):
@@ -29,7 +29,16 @@ class Camera(C.Structure):
 
 class Gaussians(C.Structure):
     _fields_ = [("count", C.c_int64), ("means", C.c_void_p), ("quats", C.c_void_p), ("scales", C.c_void_p),
-                ("opacities", C.c_void_p), ("sh", C.c_void_p), ("sh_degree", C.c_int32)]
+                ("opacities", C.c_void_p), ("sh", C.c_void_p), ("sh_degree", C.c_int32), ("cov3d", C.c_void_p)]
+
+
+class Binding(C.Structure):
+    _fields_ = [("count", C.c_int64), ("anchors", C.c_int32), ("face", C.c_void_p), ("bary", C.c_void_p)]
+
+
+class VertexField(C.Structure):
+    _fields_ = [("num_vertices", C.c_int64), ("num_faces", C.c_int64), ("faces", C.c_void_p), ("delta", C.c_void_p),
+                ("log_rot", C.c_void_p), ("shear", C.c_void_p)]
 
 
 class Mesh(C.Structure):
@@ -78,6 +87,8 @@ def load():
     L.unimgs_get_bins.argtypes = [vp, vp, vp, vp, vp]
     L.unimgs_get_records.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.unimgs_render_host.argtypes = [vp, C.POINTER(Gaussians), C.POINTER(Mesh), C.POINTER(Camera), i32, vp, vp]
+    L.unimgs_deform.argtypes = [C.POINTER(Gaussians), C.POINTER(Binding), C.POINTER(VertexField), vp, vp, vp]
+    L.unimgs_deform.restype = C.c_int
     L.unimgs_launch_count.argtypes = [vp]
     L.unimgs_launch_count.restype = i64
     L.unimgs_error_string.argtypes = [vp]

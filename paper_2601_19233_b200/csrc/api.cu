@@ -225,10 +225,10 @@ extern "C" int unimgs_preprocess(unimgs_ctx *c, const unimgs_gaussians *g, const
     if (g && g->count > 0) {
         if (g->count > c->max_g) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "gaussian count %lld above reserved %lld",
                                              (long long)g->count, (long long)c->max_g);
-        if (!g->means || !g->quats || !g->scales || !g->opacities || !g->sh)
+        if (!g->means || (!g->cov3d && (!g->quats || !g->scales)) || !g->opacities || !g->sh)
             return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "gaussian array is NULL");
         if (g->sh_degree < 0 || g->sh_degree > 3) return fail(c, UNIMGS_ERR_UNSUPPORTED, "sh_degree must be 0..3");
-        gi = GaussInput{g->count, g->means, g->quats, g->scales, g->opacities, g->sh, g->sh_degree};
+        gi = GaussInput{g->count, g->means, g->quats, g->scales, g->opacities, g->sh, g->sh_degree, g->cov3d};
     } else if (g && g->count < 0) {
         return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "negative gaussian count");
     }
@@ -297,6 +297,21 @@ extern "C" int unimgs_render_counted(unimgs_ctx *c, float *out, int64_t *work_ho
     CUDA_TRY(c, cudaStreamSynchronize(s));
     for (int k = 0; k < 4; k++) work_host[k] = (int64_t)w[k];
     return UNIMGS_OK;
+}
+
+extern "C" int unimgs_deform(const unimgs_gaussians *rest, const unimgs_binding *b, const unimgs_vertex_field *f,
+                             float *means_out, float *cov_out, void *stream) {
+    if (!rest || !b || !f || !means_out || !cov_out) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (rest->count < 0 || b->count != rest->count) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (rest->count == 0) return UNIMGS_OK;
+    if (b->anchors < 1 || b->anchors > 8) return UNIMGS_ERR_UNSUPPORTED;
+    if (!rest->means || (!rest->cov3d && (!rest->quats || !rest->scales)) || !b->face || !b->bary || !f->faces ||
+        !f->delta || !f->log_rot || !f->shear || f->num_faces < 0 || f->num_vertices < 1)
+        return UNIMGS_ERR_INVALID_ARGUMENT;
+    DeformInput d{rest->count, rest->means, rest->quats, rest->scales, rest->cov3d, b->anchors, b->face, b->bary,
+                  f->num_faces, f->faces, f->delta, f->log_rot, f->shear};
+    launch_deform(d, means_out, cov_out, (cudaStream_t)stream);
+    return cudaGetLastError() == cudaSuccess ? UNIMGS_OK : UNIMGS_ERR_CUDA;
 }
 
 extern "C" int unimgs_get_stats(unimgs_ctx *c, unimgs_stats *out, void *stream) {
@@ -424,7 +439,7 @@ extern "C" int unimgs_render_host(unimgs_ctx *c, const unimgs_gaussians *gh, con
     for (int i = 0; i < 11; i++)
         if (src[i] && bytes[i]) CUDA_TRY(c, cudaMemcpyAsync(dp[i], src[i], bytes[i], cudaMemcpyHostToDevice, s));
     unimgs_gaussians gd{N, (const float *)dp[0], (const float *)dp[1], (const float *)dp[2], (const float *)dp[3],
-                        (const float *)dp[4], N ? gh->sh_degree : 0};
+                        (const float *)dp[4], N ? gh->sh_degree : 0, nullptr};
     unimgs_mesh md{V, F, (const float *)dp[5], (F && mh->uvs) ? (const float *)dp[6] : nullptr,
                    (F && mh->colors) ? (const float *)dp[7] : nullptr, (const int32_t *)dp[8], (const float *)dp[9],
                    tex ? (const uint8_t *)dp[10] : nullptr, tex ? mh->tex_width : 0, tex ? mh->tex_height : 0};

@@ -83,6 +83,18 @@ struct GaussInput {
     int64_t N;
     const float *means, *quats, *scales, *opac, *sh;
     int sh_degree;
+    const float *cov3d;  // optional [N][6]: replaces quats/scales
+};
+
+struct DeformInput {
+    int64_t N;
+    const float *means, *quats, *scales, *cov3d;
+    int K;                 // anchors per Gaussian
+    const int32_t *face;   // [N][K]
+    const float *bary;     // [N][K][3]
+    int64_t F;
+    const int32_t *faces;  // [F][3]
+    const float *delta, *log_rot, *shear;  // per vertex [V][3], [V][3], [V][6]
 };
 
 struct MeshInput {
@@ -111,6 +123,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
 int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, const CamParams &cam,
                  const BlendParams &bp, float *out, cudaStream_t s, bool count_work = false);
 int launch_tile_stats(const Buffers &b, int tiles, cudaStream_t s);
+int launch_deform(const DeformInput &d, float *mu_out, float *cov_out, cudaStream_t s);
 int launch_full_keys(const Buffers &b, uint64_t *keys, cudaStream_t s);
 
 }  // namespace unimgs

@@ -117,9 +117,11 @@ __global__ void __launch_bounds__(256) k_preprocess_gaussians(GaussInput gin, in
         uint32_t touched = 0;
         // all per-Gaussian inputs except SH are loaded up front (one round trip)
         const float mx = __ldg(gin.means + 3 * g), my = __ldg(gin.means + 3 * g + 1), mz = __ldg(gin.means + 3 * g + 2);
-        const float qw = __ldg(gin.quats + 4 * g), qx = __ldg(gin.quats + 4 * g + 1), qy = __ldg(gin.quats + 4 * g + 2),
-                    qz = __ldg(gin.quats + 4 * g + 3);
-        const float s0 = __ldg(gin.scales + 3 * g), s1 = __ldg(gin.scales + 3 * g + 1), s2 = __ldg(gin.scales + 3 * g + 2);
+        const bool qs = gin.cov3d == nullptr;
+        const float qw = qs ? __ldg(gin.quats + 4 * g) : 1.f, qx = qs ? __ldg(gin.quats + 4 * g + 1) : 0.f,
+                    qy = qs ? __ldg(gin.quats + 4 * g + 2) : 0.f, qz = qs ? __ldg(gin.quats + 4 * g + 3) : 0.f;
+        const float s0 = qs ? __ldg(gin.scales + 3 * g) : 0.f, s1 = qs ? __ldg(gin.scales + 3 * g + 1) : 0.f,
+                    s2 = qs ? __ldg(gin.scales + 3 * g + 2) : 0.f;
         const float o = __ldg(gin.opac + g);
         do {
             float pv[3];
@@ -127,6 +129,12 @@ __global__ void __launch_bounds__(256) k_preprocess_gaussians(GaussInput gin, in
             if (!(pv[2] > cam.near_z) || pv[2] > cam.far_z) break;
             const float xz = dv(pv[0], pv[2]), yz = dv(pv[1], pv[2]);          // N2
             const float u = fma_(cam.fx, xz, cam.cx), v = fma_(cam.fy, yz, cam.cy);
+            float Sig[9];
+            if (gin.cov3d) {  // given covariance (e.g. from the deformation transfer)
+                const float *cv = gin.cov3d + 6 * g;
+                Sig[0] = __ldg(cv); Sig[1] = Sig[3] = __ldg(cv + 1); Sig[2] = Sig[6] = __ldg(cv + 2);
+                Sig[4] = __ldg(cv + 3); Sig[5] = Sig[7] = __ldg(cv + 4); Sig[8] = __ldg(cv + 5);
+            } else {
             // N3
             float w = qw, x = qx, y = qy, z = qz;
             const float n2 = fma_(w, w, fma_(x, x, fma_(y, y, mul(z, z))));
@@ -143,11 +151,11 @@ __global__ void __launch_bounds__(256) k_preprocess_gaussians(GaussInput gin, in
             for (int a = 0; a < 3; a++) {
                 m[3 * a] = mul(r[3 * a], s0); m[3 * a + 1] = mul(r[3 * a + 1], s1); m[3 * a + 2] = mul(r[3 * a + 2], s2);
             }
-            float Sig[9];
 #pragma unroll
             for (int a = 0; a < 3; a++)
 #pragma unroll
                 for (int c = 0; c < 3; c++) Sig[3 * a + c] = dot3(m + 3 * a, m + 3 * c);
+            }
             float A[9], Sv[9];
 #pragma unroll
             for (int a = 0; a < 3; a++)

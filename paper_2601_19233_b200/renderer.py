@@ -31,6 +31,7 @@ class DeviceScene:
     uvs: Optional[torch.Tensor] = None
     colors: Optional[torch.Tensor] = None
     texture: Optional[torch.Tensor] = None
+    cov3d: Optional[torch.Tensor] = None  # [N, 6]: replaces quats/scales when set
 
     @property
     def num_gaussians(self) -> int:
@@ -42,7 +43,7 @@ class DeviceScene:
 
     def nbytes(self) -> int:
         ts = [self.means, self.quats, self.scales, self.opacities, self.sh, self.positions, self.faces,
-              self.opacity, self.uvs, self.colors, self.texture]
+              self.opacity, self.uvs, self.colors, self.texture, self.cov3d]
         return int(sum(t.numel() * t.element_size() for t in ts if t is not None))
 
 
@@ -53,7 +54,8 @@ def to_device(scene, device="cuda") -> DeviceScene:
         return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(device)
 
     return DeviceScene(t(g.means), t(g.quats), t(g.scales), t(g.opacities), t(g.sh), int(g.sh_degree),
-                       t(m.positions), t(m.faces.astype(np.int32)), t(m.opacity), t(m.uvs), t(m.colors), t(m.texture))
+                       t(m.positions), t(m.faces.astype(np.int32)), t(m.opacity), t(m.uvs), t(m.colors), t(m.texture),
+                       t(getattr(g, "cov3d", None)))
 
 
 def to_pinned(scene) -> DeviceScene:
@@ -91,6 +93,7 @@ def c_gaussians(s: DeviceScene) -> _lib.Gaussians:
     g.count = s.num_gaussians
     g.means, g.quats, g.scales = _ptr(s.means), _ptr(s.quats), _ptr(s.scales)
     g.opacities, g.sh, g.sh_degree = _ptr(s.opacities), _ptr(s.sh), int(s.sh_degree)
+    g.cov3d = _ptr(s.cov3d)
     return g
 
 
@@ -242,6 +245,26 @@ class Renderer:
 
     def launch_count(self) -> int:
         return int(self.L.unimgs_launch_count(self._h))
+
+
+def deform(scene: DeviceScene, face: torch.Tensor, bary: torch.Tensor, faces: torch.Tensor, delta: torch.Tensor,
+           log_rot: torch.Tensor, shear: torch.Tensor, stream=None):
+    """Eq.12-13 on the device: returns (means' [N,3], cov' [N,6]) CUDA tensors.
+    face [N,K] int32, bary [N,K,3], faces [F,3] int32, delta/log_rot [V,3], shear [V,6]."""
+    L = _lib.load()
+    N = scene.num_gaussians
+    mo = torch.empty((N, 3), dtype=torch.float32, device=scene.means.device)
+    co = torch.empty((N, 6), dtype=torch.float32, device=scene.means.device)
+    b = _lib.Binding()
+    b.count, b.anchors, b.face, b.bary = N, int(face.shape[1]), _ptr(face), _ptr(bary)
+    f = _lib.VertexField()
+    f.num_vertices, f.num_faces = int(delta.shape[0]), int(faces.shape[0])
+    f.faces, f.delta, f.log_rot, f.shear = _ptr(faces), _ptr(delta), _ptr(log_rot), _ptr(shear)
+    rc = L.unimgs_deform(C.byref(c_gaussians(scene)), C.byref(b), C.byref(f), C.c_void_p(mo.data_ptr()),
+                         C.c_void_p(co.data_ptr()), _stream_handle(stream))
+    if rc != _lib.OK:
+        raise _lib.UnimgsError(rc, "deform")
+    return mo, co
 
 
 def estimate_pairs(scene, slack: float = 2.0, minimum: int = 1 << 16) -> int:

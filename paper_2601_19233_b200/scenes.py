@@ -455,3 +455,74 @@ def make_edge(W=64, H=64) -> Scene:
     mesh = Mesh(P.astype(np.float32), faces.astype(np.int32), np.ones(len(faces), np.float32),
                 colors=colors.astype(np.float32))
     return Scene("edge", empty_gaussians(0), mesh, [cam], bg=np.array([0.0, 0.0, 0.3], np.float32))
+
+
+# ----------------------------------------------------------------------------
+# deformation inputs (Eq.12-13): a bound proxy mesh
+# and a per-vertex transform field.  Synthetic: random nearby faces with Dirichlet
+# barycentrics stand in for the ray-cast binding; a twist/bend field stands in for
+# ACAP (out of scope).
+# ----------------------------------------------------------------------------
+
+@dataclass
+class Binding:
+    face: np.ndarray   # i32 [N, K]; < 0 = unbound anchor
+    bary: np.ndarray   # f32 [N, K, 3] (u, v, w)
+
+    @property
+    def anchors(self) -> int:
+        return int(self.face.shape[1])
+
+
+@dataclass
+class VertexField:
+    delta: np.ndarray    # f32 [V, 3]  V' - V
+    log_rot: np.ndarray  # f32 [V, 3]  axis-angle log of the vertex rotation
+    shear: np.ndarray    # f32 [V, 6]  symmetric shear: xx xy xz yy yz zz
+
+
+def make_binding(rng, gaussians: Gaussians, mesh: Mesh, K: int = 8, unbound_frac: float = 0.02,
+                 candidates: int = 16) -> Binding:
+    from scipy.spatial import cKDTree
+    P = mesh.positions.astype(np.float64)
+    cent = P[mesh.faces].mean(1)
+    tree = cKDTree(cent)
+    _, nn = tree.query(gaussians.means.astype(np.float64), k=min(candidates, len(cent)))
+    nn = np.atleast_2d(nn)
+    n = gaussians.count
+    pick = rng.integers(0, nn.shape[1], (n, K))
+    face = np.take_along_axis(nn, pick, 1).astype(np.int32)
+    face[rng.uniform(0, 1, (n, K)) < unbound_frac] = -1
+    bary = rng.dirichlet(np.ones(3), (n, K)).astype(np.float32)
+    return Binding(face, bary)
+
+
+def twist_field(mesh: Mesh, twist: float = 0.8, bend: float = 0.3, shear_eps: float = 0.05) -> VertexField:
+    """Rotation about +y by twist * y plus a bend about +z by bend * x; small smooth shear."""
+    P = mesh.positions.astype(np.float64)
+    w = np.stack([np.zeros(len(P)), twist * P[:, 1], bend * P[:, 0]], -1)
+    from scipy.spatial.transform import Rotation
+    Rm = Rotation.from_rotvec(w).as_matrix()
+    Pn = np.einsum("nij,nj->ni", Rm, P)
+    s = shear_eps * np.stack([np.sin(P[:, 0]), 0.3 * np.cos(P[:, 1]), 0.2 * np.sin(P[:, 2]),
+                              np.cos(P[:, 2]), 0.1 * np.sin(P[:, 0] + P[:, 1]), np.sin(P[:, 1])], -1)
+    shear = np.array([1, 0, 0, 1, 0, 1], np.float64) + s
+    return VertexField((Pn - P).astype(np.float32), w.astype(np.float32), shear.astype(np.float32))
+
+
+def uniform_field(V: int, delta=(0, 0, 0), log_rot=(0, 0, 0), shear=(1, 0, 0, 1, 0, 1)) -> VertexField:
+    return VertexField(np.tile(np.asarray(delta, np.float32), (V, 1)), np.tile(np.asarray(log_rot, np.float32), (V, 1)),
+                       np.tile(np.asarray(shear, np.float32), (V, 1)))
+
+
+def make_deform(seed=6, n_gauss=20000, K=8, W=160, H=120, lon=48, lat=24):
+    """Gaussians on a sphere shell bound to a UV-sphere proxy mesh (K anchors each)."""
+    rng = np.random.default_rng(seed)
+    p, uv, f = uv_sphere((0, 0, 0), 1.0, lon, lat)
+    mesh = merge_meshes([(p, uv, f, 1.0)], procedural_texture(rng, 64, 8))
+    means = _shell_points(rng, n_gauss, 1.0) * 0.98
+    scales = _lognormal_scales(rng, n_gauss, 0.02, 0.4)
+    g = _pack_gaussians(means, _quats(rng, n_gauss), scales, _opacities(rng, n_gauss), _sh(rng, n_gauss, 1), 1)
+    cam = look_at((0.0, 0.6, 3.4), width=W, height=H, fx=W * 0.9, fy=W * 0.9, cx=W / 2, cy=H / 2)
+    binding = make_binding(rng, g, mesh, K)
+    return Scene("deform", g, mesh, [cam], bg=np.array([0.1, 0.1, 0.1], np.float32)), binding
