@@ -106,13 +106,14 @@ typedef struct {
 } unimgs_binding;
 
 /* Per-vertex transforms of the manipulated proxy mesh (from ACAP or
- * any mesh deformer): delta [V][3] = V' - V, log_rot [V][3] the rotation as an
- * axis-angle vector, shear [V][6] the symmetric shear S (xx xy xz yy yz zz);
- * faces [F][3] of the rest mesh. */
+ * any mesh deformer), one 48-byte record per vertex: data [V][12] float =
+ * delta xyz (V' - V), log_rot xyz (the rotation as an axis-angle vector),
+ * shear xx xy xz yy yz zz (symmetric S); 16-byte aligned.  faces [F][3] of the
+ * rest mesh. */
 typedef struct {
     int64_t num_vertices, num_faces;
     const int32_t *faces;
-    const float *delta, *log_rot, *shear;
+    const float *data;
 } unimgs_vertex_field;
 
 /* Triangle mesh with a per-triangle opacity (reading R13).

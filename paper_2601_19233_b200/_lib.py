@@ -37,8 +37,7 @@ class Binding(C.Structure):
 
 
 class VertexField(C.Structure):
-    _fields_ = [("num_vertices", C.c_int64), ("num_faces", C.c_int64), ("faces", C.c_void_p), ("delta", C.c_void_p),
-                ("log_rot", C.c_void_p), ("shear", C.c_void_p)]
+    _fields_ = [("num_vertices", C.c_int64), ("num_faces", C.c_int64), ("faces", C.c_void_p), ("data", C.c_void_p)]
 
 
 class Mesh(C.Structure):

@@ -306,10 +306,11 @@ extern "C" int unimgs_deform(const unimgs_gaussians *rest, const unimgs_binding 
     if (rest->count == 0) return UNIMGS_OK;
     if (b->anchors < 1 || b->anchors > 8) return UNIMGS_ERR_UNSUPPORTED;
     if (!rest->means || (!rest->cov3d && (!rest->quats || !rest->scales)) || !b->face || !b->bary || !f->faces ||
-        !f->delta || !f->log_rot || !f->shear || f->num_faces < 0 || f->num_vertices < 1)
+        !f->data || f->num_faces < 0 || f->num_vertices < 1)
         return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (reinterpret_cast<uintptr_t>(f->data) & 15) return UNIMGS_ERR_INVALID_ARGUMENT;
     DeformInput d{rest->count, rest->means, rest->quats, rest->scales, rest->cov3d, b->anchors, b->face, b->bary,
-                  f->num_faces, f->faces, f->delta, f->log_rot, f->shear};
+                  f->num_faces, f->faces, reinterpret_cast<const float4 *>(f->data)};
     launch_deform(d, means_out, cov_out, (cudaStream_t)stream);
     return cudaGetLastError() == cudaSuccess ? UNIMGS_OK : UNIMGS_ERR_CUDA;
 }

@@ -41,17 +41,18 @@ __global__ void __launch_bounds__(256) k_deform(DeformInput d, float *__restrict
         const int f = __ldg(d.face + g * d.K + i);
         if (f < 0 || f >= d.F) continue;
         const float *bw = d.bary + 3 * (g * d.K + i);
+        const float b3[3] = {__ldg(bw), __ldg(bw + 1), __ldg(bw + 2)};
+        const int v3[3] = {__ldg(d.faces + 3 * (int64_t)f), __ldg(d.faces + 3 * (int64_t)f + 1),
+                           __ldg(d.faces + 3 * (int64_t)f + 2)};
 #pragma unroll
         for (int j = 0; j < 3; j++) {
-            const int64_t v = __ldg(d.faces + 3 * (int64_t)f + j);
-            const float wj = __ldg(bw + j);
-#pragma unroll
-            for (int a = 0; a < 3; a++) {
-                sd[a] += wj * __ldg(d.delta + 3 * v + a);
-                sl[a] += wj * __ldg(d.log_rot + 3 * v + a);
-            }
-#pragma unroll
-            for (int a = 0; a < 6; a++) ss[a] += wj * __ldg(d.shear + 6 * v + a);
+            const float4 *vp = d.vdata + 3 * (int64_t)v3[j];
+            const float4 p0 = __ldg(vp), p1 = __ldg(vp + 1), p2 = __ldg(vp + 2);
+            const float wj = b3[j];
+            sd[0] += wj * p0.x; sd[1] += wj * p0.y; sd[2] += wj * p0.z;
+            sl[0] += wj * p0.w; sl[1] += wj * p1.x; sl[2] += wj * p1.y;
+            ss[0] += wj * p1.z; ss[1] += wj * p1.w; ss[2] += wj * p2.x;
+            ss[3] += wj * p2.y; ss[4] += wj * p2.z; ss[5] += wj * p2.w;
         }
         n++;
     }

@@ -94,7 +94,7 @@ struct DeformInput {
     const float *bary;     // [N][K][3]
     int64_t F;
     const int32_t *faces;  // [F][3]
-    const float *delta, *log_rot, *shear;  // per vertex [V][3], [V][3], [V][6]
+    const float4 *vdata;   // per vertex 3 x float4: delta xyz + log_rot x | log_rot yz + shear xx xy | shear xz yy yz zz
 };
 
 struct MeshInput {

@@ -247,10 +247,10 @@ class Renderer:
         return int(self.L.unimgs_launch_count(self._h))
 
 
-def deform(scene: DeviceScene, face: torch.Tensor, bary: torch.Tensor, faces: torch.Tensor, delta: torch.Tensor,
-           log_rot: torch.Tensor, shear: torch.Tensor, stream=None):
+def deform(scene: DeviceScene, face: torch.Tensor, bary: torch.Tensor, faces: torch.Tensor, vdata: torch.Tensor,
+           stream=None):
     """Eq.12-13 on the device: returns (means' [N,3], cov' [N,6]) CUDA tensors.
-    face [N,K] int32, bary [N,K,3], faces [F,3] int32, delta/log_rot [V,3], shear [V,6]."""
+    face [N,K] int32, bary [N,K,3], faces [F,3] int32, vdata [V,12] (VertexField.packed())."""
     L = _lib.load()
     N = scene.num_gaussians
     mo = torch.empty((N, 3), dtype=torch.float32, device=scene.means.device)
@@ -258,8 +258,8 @@ def deform(scene: DeviceScene, face: torch.Tensor, bary: torch.Tensor, faces: to
     b = _lib.Binding()
     b.count, b.anchors, b.face, b.bary = N, int(face.shape[1]), _ptr(face), _ptr(bary)
     f = _lib.VertexField()
-    f.num_vertices, f.num_faces = int(delta.shape[0]), int(faces.shape[0])
-    f.faces, f.delta, f.log_rot, f.shear = _ptr(faces), _ptr(delta), _ptr(log_rot), _ptr(shear)
+    f.num_vertices, f.num_faces = int(vdata.shape[0]), int(faces.shape[0])
+    f.faces, f.data = _ptr(faces), _ptr(vdata)
     rc = L.unimgs_deform(C.byref(c_gaussians(scene)), C.byref(b), C.byref(f), C.c_void_p(mo.data_ptr()),
                          C.c_void_p(co.data_ptr()), _stream_handle(stream))
     if rc != _lib.OK:

@@ -480,18 +480,26 @@ class VertexField:
     log_rot: np.ndarray  # f32 [V, 3]  axis-angle log of the vertex rotation
     shear: np.ndarray    # f32 [V, 6]  symmetric shear: xx xy xz yy yz zz
 
+    def packed(self) -> np.ndarray:
+        """[V, 12] float32: delta xyz, log_rot xyz, shear xx xy xz yy yz zz (the C ABI layout)."""
+        return np.ascontiguousarray(np.concatenate([self.delta, self.log_rot, self.shear], 1), np.float32)
+
 
 def make_binding(rng, gaussians: Gaussians, mesh: Mesh, K: int = 8, unbound_frac: float = 0.02,
-                 candidates: int = 16) -> Binding:
-    from scipy.spatial import cKDTree
+                 spread: int = 8, nearest: bool = True) -> Binding:
+    """Each anchor: the face nearest to the Gaussian (by centroid) shifted by a random index
+    offset in [-spread, spread] (grid meshes: index neighbours are spatial neighbours).
+    nearest=False draws the base face uniformly (large scenes whose Gaussians lie far from
+    the mesh, where exact nearest-face queries are slow; timing only)."""
+    n = gaussians.count
     P = mesh.positions.astype(np.float64)
     cent = P[mesh.faces].mean(1)
-    tree = cKDTree(cent)
-    _, nn = tree.query(gaussians.means.astype(np.float64), k=min(candidates, len(cent)))
-    nn = np.atleast_2d(nn)
-    n = gaussians.count
-    pick = rng.integers(0, nn.shape[1], (n, K))
-    face = np.take_along_axis(nn, pick, 1).astype(np.int32)
+    if nearest:
+        from scipy.spatial import cKDTree
+        _, nn = cKDTree(cent).query(gaussians.means.astype(np.float64), k=1)
+    else:
+        nn = rng.integers(0, len(cent), n)
+    face = np.clip(nn[:, None] + rng.integers(-spread, spread + 1, (n, K)), 0, len(cent) - 1).astype(np.int32)
     face[rng.uniform(0, 1, (n, K)) < unbound_frac] = -1
     bary = rng.dirichlet(np.ones(3), (n, K)).astype(np.float32)
     return Binding(face, bary)

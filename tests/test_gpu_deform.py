@@ -16,7 +16,7 @@ def _gpu_deform(sc, b, field):
     from paper_2601_19233_b200 import renderer as R
     ds = R.to_device(sc)
     mo, co = R.deform(ds, _dev(b.face, np.int32), _dev(b.bary, np.float32), _dev(sc.mesh.faces, np.int32),
-                      _dev(field.delta), _dev(field.log_rot), _dev(field.shear))
+                      _dev(field.packed()))
     return ds, mo.cpu().numpy(), co.cpu().numpy()
 
 
