@@ -127,7 +127,7 @@ extern "C" int unimgs_set_settings(unimgs_ctx *c, const unimgs_settings *s) {
 static void free_buffers(unimgs_ctx *c) {
     Buffers &b = c->buf;
     void *ptrs[] = {b.rect, b.touched, b.dkey, b.grec, b.trec, b.pk[0], b.pk[1], b.pv[0], b.pv[1], b.tk[0], b.tk[1],
-                    b.tv[0], b.tv[1], b.ranges, b.bcnt, b.dcnt, b.lookback, b.st};
+                    b.tv[0], b.tv[1], b.ranges, b.order, b.bcnt, b.dcnt, b.lookback, b.st};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     memset(&b, 0, sizeof b);
@@ -159,6 +159,7 @@ extern "C" int unimgs_reserve2(unimgs_ctx *c, int64_t max_gaussians, int64_t max
         CUDA_TRY(c, cudaMalloc(&b.tv[i], sizeof(uint32_t) * max_pairs));
     }
     CUDA_TRY(c, cudaMalloc(&b.ranges, sizeof(uint2) * tiles));
+    CUDA_TRY(c, cudaMalloc(&b.order, sizeof(uint32_t) * tiles));
     CUDA_TRY(c, cudaMalloc(&b.bcnt, sizeof(uint32_t) * (size_t)(max_gaussians / 256 + max_triangles / 256 + 4)));
     CUDA_TRY(c, cudaMalloc(&b.dcnt, sizeof(uint32_t) * (size_t)(P / 2048 + 4)));
     CUDA_TRY(c, cudaMalloc(&b.lookback, sizeof(unsigned long long) * 256 * lb_tiles));

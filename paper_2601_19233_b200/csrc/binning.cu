@@ -652,6 +652,43 @@ static void set_attrs() {
     done = true;
 }
 
+// Blend schedule (longest first): the hardware hands out CTAs in blockIdx order,
+// so listing the tiles by decreasing pair count lets the few heavy tiles start in
+// the first wave instead of forming the tail.  Counting sort on an 8-bit
+// log-scale bucket (fp32 exponent + 3 mantissa bits of the count); the order
+// within a bucket is arbitrary (each tile's pixels do not depend on it).
+__global__ void __launch_bounds__(1024) k_tile_order(const uint2 *__restrict__ ranges, int tiles, uint32_t *order,
+                                                     const DevState *st) {
+    __shared__ unsigned s_h[256];
+    if (st->overflow) return;
+    auto bucket = [](const uint2 r) {
+        const unsigned len = r.y - r.x;
+        if (!len) return 0u;
+        return min(255u, (__float_as_uint((float)len) >> 20) - 1015u);  // 1..201 for len < 2^24
+    };
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_h[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < tiles; i += blockDim.x) atomicAdd(&s_h[bucket(ranges[i])], 1u);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan from the heaviest bucket down
+        unsigned carry = 0;
+        for (int c = 7; c >= 0; c--) {
+            const int k = c * 32 + (31 - (int)threadIdx.x);  // lane 0 = highest bucket of the chunk
+            const unsigned v = s_h[k];
+            unsigned x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+                if ((int)threadIdx.x >= o) x += y;
+            }
+            s_h[k] = carry + x - v;
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < tiles; i += blockDim.x) order[atomicAdd(&s_h[bucket(ranges[i])], 1u)] = (uint32_t)i;
+}
+
 int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam, int sort_mode, cudaStream_t s,
                int sm_count) {
     (void)N; (void)F;
@@ -725,6 +762,8 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
     }
     b.sorted_keys = b.tk[tc];
     b.sorted_vals = b.tv[tc];
+    k_tile_order<<<1, 1024, 0, s>>>(b.ranges, (int)tiles, b.order, b.st);
+    launches++;
     return launches;  // kernels only (the ranges memset is not counted)
 }
 

@@ -253,6 +253,7 @@ __device__ __forceinline__ void tri_pixel(Px<MODE, M> &s, const TriRecord &r, in
 #endif
 template <bool COUNT, int PIX, int MODE, int M>
 __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blend(const uint2 *__restrict__ ranges,
+                                                                     const uint32_t *__restrict__ order,
                                                                      const uint32_t *__restrict__ vals,
                                                                      const GaussRecord *__restrict__ grec,
                                                                      const TriRecord *__restrict__ trec, TexView tv,
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
     __shared__ float4 s_buf[NW][32][3];  // per-warp packed entries: a (u, v, q_max, o), (ca, 2cb, cc, id), c
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tile = blockIdx.x;
+    const int tile = (int)__ldg(order + blockIdx.x);  // longest-first schedule (k_tile_order)
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int sx0 = tx * kTile + (warp & 1) * 8, sy0 = ty * kTile + (warp >> 1) * 4 * PIX;
     const int x = sx0 + (lane & 7), y0 = sy0 + (lane >> 3);
@@ -432,11 +433,11 @@ static void launch_mode(const Buffers &b, const MeshInput &m, const CamParams &c
     const int tiles = cam.tiles_x * cam.tiles_y;
     TexView tv{reinterpret_cast<const uchar4 *>(m.tex), m.tw, m.th};
     if (count_work)
-        k_blend<true, PIX, MODE, M><<<tiles, kBlendThreads / PIX, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv,
+        k_blend<true, PIX, MODE, M><<<tiles, kBlendThreads / PIX, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
                                                                         (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
                                                                         reinterpret_cast<float4 *>(out), b.st);
     else
-        k_blend<false, PIX, MODE, M><<<tiles, kBlendThreads / PIX, 0, s>>>(b.ranges, b.sorted_vals, b.grec, b.trec, tv,
+        k_blend<false, PIX, MODE, M><<<tiles, kBlendThreads / PIX, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
                                                                          (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
                                                                          reinterpret_cast<float4 *>(out), b.st);
 }

@@ -69,6 +69,7 @@ struct Buffers {
     void *tk[2];          // pair keys ping-pong (uint16 tile ids, or uint64 full keys) [max_pairs]
     uint32_t *tv[2];      // pair values ping-pong [max_pairs]
     uint2 *ranges;        // [tiles]
+    uint32_t *order;      // [tiles] blend schedule: tiles by decreasing pair count (approx., k_tile_order)
     uint32_t *bcnt;       // per-CTA visible counts of B2 then B1 (256 primitives each), scanned in place
     uint32_t *dcnt;       // per-CTA pair counts of the duplication (2048 primitives each), scanned in place
     unsigned long long *lookback;  // [max_lb_tiles][256]
