@@ -40,7 +40,8 @@ class CCamera(C.Structure):
 
 class CSettings(C.Structure):
     _fields_ = [("alpha_max", C.c_float), ("t_eps", C.c_float), ("dilation", C.c_float),
-                ("bg", C.c_float * 3), ("bg_alpha", C.c_float), ("blend_mode", C.c_int32), ("msaa", C.c_int32)]
+                ("bg", C.c_float * 3), ("bg_alpha", C.c_float), ("blend_mode", C.c_int32), ("msaa", C.c_int32),
+                ("tri_depth", C.c_int32)]
 
 
 # blend modes: the paper's ablation (Fig.3 / Fig.4)
@@ -101,6 +102,8 @@ def lib():
         L.or_deform.restype = i32
         L.or_rodrigues_public.argtypes = [vp, vp]
         L.or_rodrigues_public.restype = None
+        L.or_tri_tile_depth.argtypes = [vp, i64, i32, i32]
+        L.or_tri_tile_depth.restype = C.c_float
         _lib = L
     return _lib
 
@@ -110,10 +113,11 @@ def _ptr(a: Optional[np.ndarray]):
 
 
 def make_settings(alpha_max=0.99, t_eps=1e-4, dilation=0.3, bg=(0.0, 0.0, 0.0), bg_alpha=1.0, blend_mode=EXACT,
-                  msaa=4) -> CSettings:
+                  msaa=4, tri_depth=0) -> CSettings:
+    """tri_depth: 0 = centroid sort depth (R9), 1 = plane depth at the tile centre (N8)."""
     s = CSettings()
     s.alpha_max, s.t_eps, s.dilation, s.bg_alpha = alpha_max, t_eps, dilation, bg_alpha
-    s.blend_mode, s.msaa = blend_mode, msaa
+    s.blend_mode, s.msaa, s.tri_depth = blend_mode, msaa, tri_depth
     for i in range(3):
         s.bg[i] = float(bg[i])
     return s
@@ -220,6 +224,10 @@ class Oracle:
         lib().or_get_triangle_records(self._h, _ptr(out["xy"]), _ptr(out["vid"]), _ptr(out["z"]),
                                       _ptr(out["depth"]), _ptr(out["rect"]), _ptr(out["touched"]))
         return out
+
+    def tri_tile_depth(self, f: int, tx: int, ty: int) -> np.float32:
+        """N8: sort depth of triangle f in tile (tx, ty) (after project())."""
+        return np.float32(lib().or_tri_tile_depth(self._h, int(f), int(tx), int(ty)))
 
     def bins(self):
         keys = np.zeros(self.K, np.uint64)

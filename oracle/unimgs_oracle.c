@@ -53,6 +53,7 @@ typedef struct {
     float bg_alpha;
     int32_t blend_mode; /* OR_EXACT .. OR_PAPER_LITERAL */
     int32_t msaa;       /* M in {1, 2, 4, 8, 16} (P:330 uses 4) */
+    int32_t tri_depth;  /* triangle sort depth: 0 = centroid (R9), 1 = plane depth at the tile centre (N8, NEXT 3) */
 } or_settings;
 
 typedef struct {
@@ -383,6 +384,36 @@ int or_project(or_ctx *c, const or_camera *cam, const or_settings *set, int nthr
 /* ------------------------------------------------------------------------- */
 /* Binning: one key per (tile, primitive) = tile<<32 | bits(depth); sort (key, id). */
 
+/* N8 ("incorporate triangle fragments into the
+ * depth-sorting process"): the per-tile sort depth of triangle f in tile (tx, ty) is
+ * the view z of its plane at the tile centre, clamped to the triangle's z range.
+ * 1/z is affine in screen space, so with the exact integer edge functions E_k of
+ * N7 at the tile centre P and A2 = 2 x area:  1/z(P) = sum_k (E_k(P) / A2) / z_k.
+ * Evaluated in double, in this order:  w_k = E_k / z_k;  s = (w_0 + w_1) + w_2;
+ * z = (float)(A2 / s), clamped to [min z_k, max z_k];  s <= 0 (the plane's
+ * horizon lies between P and the triangle) gives max z_k.                     */
+float or_tri_tile_depth(const or_ctx *c, int64_t f, int tx, int ty) {
+    const int32_t *xy = c->t_xy + 6 * f;
+    const float *z = c->t_z + 3 * f;
+    const int64_t PX = 4096 * (int64_t)tx + 2048, PY = 4096 * (int64_t)ty + 2048;
+    int64_t E[3];
+    for (int k = 0; k < 3; k++) {
+        const int a = (k + 1) % 3, b = (k + 2) % 3;
+        const int64_t Xa = xy[2 * a], Ya = xy[2 * a + 1], Xb = xy[2 * b], Yb = xy[2 * b + 1];
+        E[k] = (Xb - Xa) * (PY - Ya) - (Yb - Ya) * (PX - Xa);
+    }
+    const int64_t A2 = (int64_t)(xy[2] - xy[0]) * (xy[5] - xy[1]) - (int64_t)(xy[4] - xy[0]) * (xy[3] - xy[1]);
+    const double s = ((double)E[0] / (double)z[0] + (double)E[1] / (double)z[1]) + (double)E[2] / (double)z[2];
+    const float zmin = fminf(fminf(z[0], z[1]), z[2]), zmax = fmaxf(fmaxf(z[0], z[1]), z[2]);
+    if (!(s > 0.0)) return zmax;
+    return fminf(fmaxf((float)((double)A2 / s), zmin), zmax);
+}
+
+/* sort depth of triangle f for the tile holding (tx, ty) (R9 or N8) */
+static float tri_key_depth(const or_ctx *c, int64_t f, int tx, int ty) {
+    return c->set.tri_depth == 1 ? or_tri_tile_depth(c, f, tx, ty) : c->t_depth[f];
+}
+
 static float prim_depth(const or_ctx *c, uint32_t id) {
     return (int64_t)id < c->F ? c->t_depth[id] : c->g_rec[8 * ((int64_t)id - c->F) + 7];
 }
@@ -413,11 +444,12 @@ int64_t or_bin(or_ctx *c) {
         const int32_t *rect = p < F ? c->t_rect + 4 * p : c->g_rect + 4 * (p - F);
         uint32_t touched = p < F ? c->t_touched[p] : c->g_touched[p - F];
         if (!touched) continue;
-        uint32_t db = f32_bits(prim_depth(c, (uint32_t)p));
+        const uint32_t db = f32_bits(prim_depth(c, (uint32_t)p));
         for (int ty = rect[1]; ty <= rect[3]; ty++)
             for (int tx = rect[0]; tx <= rect[2]; tx++) {
                 uint64_t tile = (uint64_t)ty * (uint64_t)c->tiles_x + (uint64_t)tx;
-                pairs[n].key = (tile << 32) | db;
+                const uint32_t d = p < F ? f32_bits(tri_key_depth(c, p, tx, ty)) : db;
+                pairs[n].key = (tile << 32) | d;
                 pairs[n].val = (uint32_t)p;
                 n++;
             }
@@ -591,7 +623,7 @@ static int triangle_fragment(const or_ctx *c, int64_t f, int x, int y, or_frag *
     fr->kind = 1;
     fr->mask = m;
     fr->q = 0.0f;
-    fr->depth = c->t_depth[f];
+    fr->depth = tri_key_depth(c, f, x / OR_TILE, y / OR_TILE);
     fr->alpha = (double)c->topac[f];
     triangle_colour(c, f, x, y, fr->rgb);
     return 1;
@@ -853,7 +885,8 @@ int or_render_supersampled(or_ctx *c, double *out, int S, int nthreads) {
                         int64_t n = 0;
                         for (int64_t f = 0; f < c->F; f++) {
                             if (!c->t_touched[f] || !or_inside(c->t_xy + 6 * f, PX, PY)) continue;
-                            buf[n].id = (uint32_t)f; buf[n].kind = 1; buf[n].mask = 1; buf[n].depth = c->t_depth[f];
+                            buf[n].id = (uint32_t)f; buf[n].kind = 1; buf[n].mask = 1;
+                            buf[n].depth = tri_key_depth(c, f, x / OR_TILE, y / OR_TILE);
                             buf[n].alpha = (double)c->topac[f];
                             triangle_colour_at(c, f, PX, PY, buf[n].rgb);
                             n++;

@@ -457,6 +457,46 @@ def make_edge(W=64, H=64) -> Scene:
     return Scene("edge", empty_gaussians(0), mesh, [cam], bg=np.array([0.0, 0.0, 0.3], np.float32))
 
 
+def make_crossing(W=128, H=96, n_gauss=0, alpha=1.0, seed=11) -> Scene:
+    """Two interpenetrating tilted quads (SURVEY §8(f) row 3, P:511-515 nested
+    relations): quad A (red) recedes from left to right, quad B (green) the
+    other way, so each is in front on one side of the crossing column x = W/2.
+    1/z is affine in screen space on each (planar) quad: 1/z_A = 0.5 - u/(2W)
+    ... (z from 2 to 4), B mirrored.  Optional random Gaussians in the frustum."""
+    fx = fy = float(W)
+    cam = Camera(W, H, fx, fy, W / 2.0, H / 2.0, np.eye(3, dtype=np.float32), np.zeros(3, np.float32))
+    u0, u1, v0, v1 = 6.0, W - 6.0, 6.0, H - 6.0
+
+    def world(u, v, z):
+        return [(u - W / 2.0) / fx * z, (v - H / 2.0) / fy * z, z]
+
+    def inv_z(u, left, right):  # 1/z affine in u between the quad's left and right edge depths
+        t = (u - u0) / (u1 - u0)
+        return (1.0 - t) / left + t / right
+
+    P, cols = [], []
+    for (zl, zr, c) in ((2.0, 4.0, (1.0, 0.1, 0.1)), (4.0, 2.0, (0.1, 1.0, 0.1))):
+        for (u, v) in ((u0, v0), (u1, v0), (u1, v1), (u0, v1)):
+            P.append(world(u, v, 1.0 / inv_z(u, zl, zr)))
+            cols.append(c)
+    faces = np.array([[0, 1, 2], [0, 2, 3], [4, 5, 6], [4, 6, 7]], np.int32)
+    mesh = Mesh(np.array(P, np.float32), faces, np.full(4, alpha, np.float32), colors=np.array(cols, np.float32))
+    g = empty_gaussians(0)
+    if n_gauss:
+        rng = np.random.default_rng(seed)
+        z = rng.uniform(1.5, 5.0, n_gauss)
+        uv = np.stack([rng.uniform(0, W, n_gauss), rng.uniform(0, H, n_gauss)], -1)
+        means = np.stack([(uv[:, 0] - W / 2) / fx * z, (uv[:, 1] - H / 2) / fy * z, z], -1)
+        q = rng.normal(size=(n_gauss, 4))
+        q /= np.linalg.norm(q, axis=1, keepdims=True)
+        sh = np.zeros((n_gauss, 1, 3))
+        sh[:, 0, :] = (rng.uniform(0.15, 0.85, (n_gauss, 3)) - 0.5) / 0.28209479
+        g = Gaussians(means.astype(np.float32), q.astype(np.float32),
+                      np.exp(rng.normal(np.log(0.03), 0.4, (n_gauss, 3))).astype(np.float32),
+                      rng.uniform(0.2, 0.95, n_gauss).astype(np.float32), sh.astype(np.float32), 0)
+    return Scene("crossing", g, mesh, [cam], bg=np.array([0.0, 0.0, 0.0], np.float32))
+
+
 # ----------------------------------------------------------------------------
 # deformation inputs (SURVEY §8(f) row 2; Eq.12-13, P:403-436): a bound proxy mesh
 # and a per-vertex transform field.  Synthetic: random nearby faces with Dirichlet
