@@ -145,13 +145,21 @@ typedef struct {
  *   2 = per-pixel MSAA with alpha, geometric coverage (Eq.5-6)
  *   3 = whole-pixel entity across Gaussians (Fig.3b-c / 4c, colour overflow)
  *   4 = exact entity with the paper-literal exit update T *= (1 - O_geo alpha)
- *       per triangle (Eq.6 as "still updated by Eq.(6)")            */
+ *       per triangle (Eq.6 as "still updated by Eq.(6)")
+ * tri_depth: the sort depth of a triangle ("incorporate triangle fragments
+ * into the depth-sorting process"):
+ *   0 = view z of its centroid, one key per triangle (reading R9, default)
+ *   1 = per (tile, triangle) pair: the view z of its plane at the tile centre,
+ *       clamped to the triangle's z range (N8) -- interpenetrating
+ *       surfaces swap order across tiles.  Per-pair keys need the full 64-bit
+ *       sort, so tri_depth 1 always bins as sort_mode 1.                     */
 typedef struct {
     int32_t msaa_samples, tile_size;
     float alpha_min, alpha_max, t_eps, dilation;
     float bg[3], bg_alpha;
     int32_t sort_mode;
     int32_t blend_mode;
+    int32_t tri_depth;
 } unimgs_settings;
 
 typedef struct {
@@ -167,7 +175,8 @@ typedef struct {
 } unimgs_stats;
 
 /* Fill *s with the defaults (M = 4, 16x16 tiles, alpha in [1/255, 0.99],
- * t_eps 1e-4, dilation 0.3, black opaque background, sort_mode 0). */
+ * t_eps 1e-4, dilation 0.3, black opaque background, sort_mode 0, blend_mode 0,
+ * tri_depth 0). */
 UNIMGS_API void unimgs_default_settings(unimgs_settings *s);
 
 /* Create a context.  s may be NULL (defaults).  No device memory yet. */

@@ -73,6 +73,8 @@ extern "C" void unimgs_default_settings(unimgs_settings *s) {
     s->dilation = 0.3f;
     s->bg_alpha = 1.0f;
     s->sort_mode = 0;
+    s->blend_mode = 0;
+    s->tri_depth = 0;
 }
 
 static int validate_settings(unimgs_ctx *c, const unimgs_settings *s) {
@@ -88,6 +90,7 @@ static int validate_settings(unimgs_ctx *c, const unimgs_settings *s) {
     if (!(s->t_eps >= 0.f && s->t_eps < 1.f)) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "t_eps not in [0,1)");
     if (!(s->dilation >= 0.f && std::isfinite(s->dilation))) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "dilation < 0");
     if (s->sort_mode != 0 && s->sort_mode != 1) return fail(c, UNIMGS_ERR_UNSUPPORTED, "sort_mode must be 0 or 1");
+    if (s->tri_depth != 0 && s->tri_depth != 1) return fail(c, UNIMGS_ERR_UNSUPPORTED, "tri_depth must be 0 or 1");
     for (int i = 0; i < 3; i++)
         if (!std::isfinite(s->bg[i])) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "bg not finite");
     if (!std::isfinite(s->bg_alpha)) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "bg_alpha not finite");
@@ -210,7 +213,7 @@ static int make_cam(unimgs_ctx *c, const unimgs_camera *cam, CamParams &cp) {
     for (int a = 0; a < 3; a++)
         cp.campos[a] = (float)(-((double)cam->R[a] * cam->t[0] + (double)cam->R[3 + a] * cam->t[1] +
                                  (double)cam->R[6 + a] * cam->t[2]));
-    if ((int64_t)cp.tiles_x * cp.tiles_y > 65536 && c->set.sort_mode == 0)
+    if ((int64_t)cp.tiles_x * cp.tiles_y > 65536 && c->set.sort_mode == 0 && c->set.tri_depth == 0)
         return fail(c, UNIMGS_ERR_UNSUPPORTED, "sort_mode 0 supports at most 65536 tiles; use sort_mode 1");
     return UNIMGS_OK;
 }
@@ -264,8 +267,9 @@ extern "C" int unimgs_preprocess(unimgs_ctx *c, const unimgs_gaussians *g, const
 extern "C" int unimgs_bin(unimgs_ctx *c, void *stream) {
     if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
     if (c->stage < 1) return fail(c, UNIMGS_ERR_STATE, "bin before preprocess");
-    c->sort_mode_used = c->set.sort_mode;
-    c->launches += launch_bin(c->buf, c->P, c->g.N, c->m.F, c->cam, c->set.sort_mode, (cudaStream_t)stream, c->sm_count);
+    c->sort_mode_used = c->set.tri_depth ? 1 : c->set.sort_mode;  // per-pair triangle keys need the full sort
+    c->launches += launch_bin(c->buf, c->P, c->g.N, c->m.F, c->cam, c->sort_mode_used, c->set.tri_depth,
+                              (cudaStream_t)stream, c->sm_count);
     int rc = check_launch(c, "bin");
     if (rc) return rc;
     c->stage = 2;

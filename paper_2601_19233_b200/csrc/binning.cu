@@ -275,13 +275,34 @@ struct DupCfg {
     using Key = typename std::conditional<FULL, unsigned long long, uint16_t>::type;
 };
 
+// N8: bits of triangle f's sort depth in tile
+// (tx, ty) -- the view z of its plane at the tile centre, clamped to its z range.
+// 1/z is affine in screen space: 1/z(P) = sum_k (E_k(P) / A2) / z_k with the
+// exact integer edge functions of N7.  Normative order, in double:
+// w_k = E_k / z_k; s = (w_0 + w_1) + w_2; z = (float)(A2 / s); s <= 0 -> max z.
+__device__ __forceinline__ uint32_t tile_plane_depth_bits(const int4 q0, const int4 q1, const float4 q2, unsigned tx,
+                                                          unsigned ty) {
+    const long long PX = 4096ll * tx + 2048, PY = 4096ll * ty + 2048;
+    const long long X0 = q0.x, Y0 = q0.y, X1 = q0.z, Y1 = q0.w, X2 = q1.x, Y2 = q1.y;
+    const long long E0 = (X2 - X1) * (PY - Y1) - (Y2 - Y1) * (PX - X1);
+    const long long E1 = (X0 - X2) * (PY - Y2) - (Y0 - Y2) * (PX - X2);
+    const long long E2 = (X1 - X0) * (PY - Y0) - (Y1 - Y0) * (PX - X0);
+    const long long A2 = (X1 - X0) * (Y2 - Y0) - (X2 - X0) * (Y1 - Y0);
+    const double s = __dadd_rn(__dadd_rn(__ddiv_rn((double)E0, (double)q2.x), __ddiv_rn((double)E1, (double)q2.y)),
+                               __ddiv_rn((double)E2, (double)q2.z));
+    const float zmin = fminf(fminf(q2.x, q2.y), q2.z), zmax = fmaxf(fmaxf(q2.x, q2.y), q2.z);
+    if (!(s > 0.0)) return __float_as_uint(zmax);
+    return __float_as_uint(fminf(fmaxf(__double2float_rn(__ddiv_rn((double)A2, s)), zmin), zmax));
+}
+
 template <bool FULL>
 __global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t *__restrict__ ids,
                                                             const uint32_t *__restrict__ touched,
                                                             const uint2 *__restrict__ rect,
                                                             const uint32_t *__restrict__ dkey, int tiles_x,
                                                             int64_t cap, const uint32_t *__restrict__ doff,
-                                                            void *tk_, uint32_t *tv, DevState *st) {
+                                                            const TriRecord *__restrict__ trec, unsigned F,
+                                                            int tri_depth, void *tk_, uint32_t *tv, DevState *st) {
     using Key = typename DupCfg<FULL>::Key;
     constexpr int CAP = DupCfg<FULL>::CAP;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -331,10 +352,23 @@ __global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t *__re
             const unsigned x0 = r[i].x & 0xFFFF, y0 = r[i].x >> 16, x1 = r[i].y & 0xFFFF;
             const unsigned wdt = x1 - x0 + 1, l0 = lo - ex[i];
             unsigned tx = x0 + l0 % wdt, ty = y0 + l0 / wdt;
+            const bool plane = FULL && tri_depth && id[i] < F;  // N8 per-tile triangle depth
+            int4 tq0 = make_int4(0, 0, 0, 0), tq1 = tq0;
+            float4 tq2 = make_float4(1.f, 1.f, 1.f, 1.f);
+            if (plane) {
+                const int4 *q = reinterpret_cast<const int4 *>(trec + id[i]);
+                tq0 = __ldg(q);
+                tq1 = __ldg(q + 1);
+                tq2 = __ldg(reinterpret_cast<const float4 *>(q + 2));
+            }
             for (unsigned g = lo; g < hi; g++) {
                 const unsigned t = ty * (unsigned)tiles_x + tx;
-                if (FULL) s_k[g - wb] = (Key)(((unsigned long long)t << 32) | dk[i]);
-                else s_k[g - wb] = (Key)t;
+                if (FULL) {
+                    const uint32_t d = plane ? tile_plane_depth_bits(tq0, tq1, tq2, tx, ty) : dk[i];
+                    s_k[g - wb] = (Key)(((unsigned long long)t << 32) | d);
+                } else {
+                    s_k[g - wb] = (Key)t;
+                }
                 s_v[g - wb] = id[i];
                 if (++tx > x1) { tx = x0; ty++; }
             }
@@ -689,9 +723,9 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2 *__restrict__ r
     for (int i = threadIdx.x; i < tiles; i += blockDim.x) order[atomicAdd(&s_h[bucket(ranges[i])], 1u)] = (uint32_t)i;
 }
 
-int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam, int sort_mode, cudaStream_t s,
-               int sm_count) {
-    (void)N; (void)F;
+int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam, int sort_mode, int tri_depth,
+               cudaStream_t s, int sm_count) {
+    (void)N;
     set_attrs();
     int launches = 0;
     const int64_t tiles = (int64_t)cam.tiles_x * cam.tiles_y;
@@ -732,8 +766,8 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
     const int g2 = sort_grid(b.max_pairs, sm_count, 2);
     if (!full) {
         k_duplicate<false><<<dgrid, kScanThreads, dup_smem<false>(), s>>>(dup_ids, b.touched, b.rect, b.dkey,
-                                                                          cam.tiles_x, b.max_pairs, b.dcnt, b.tk[0],
-                                                                          b.tv[0], b.st);
+                                                                          cam.tiles_x, b.max_pairs, b.dcnt, b.trec,
+                                                                          (unsigned)F, 0, b.tk[0], b.tv[0], b.st);
         launches++;
         for (int pass = 0, sh = 0; sh < tb; pass++, sh += 8, slot++) {
             onesweep_pass<uint16_t>(b, (const uint16_t *)b.tk[tc], b.tv[tc], (uint16_t *)b.tk[tc ^ 1], b.tv[tc ^ 1],
@@ -746,7 +780,8 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         launches++;
     } else {
         k_duplicate<true><<<dgrid, kScanThreads, dup_smem<true>(), s>>>(dup_ids, b.touched, b.rect, b.dkey, cam.tiles_x,
-                                                                        b.max_pairs, b.dcnt, b.tk[0], b.tv[0], b.st);
+                                                                        b.max_pairs, b.dcnt, b.trec, (unsigned)F,
+                                                                        tri_depth, b.tk[0], b.tv[0], b.st);
         launches++;
         const int total_bits = 32 + tb;
         for (int pass = 0, sh = 0; sh < total_bits; pass++, sh += 8, slot++) {

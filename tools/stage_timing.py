@@ -21,12 +21,13 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--sort-mode", type=int, default=0)
     ap.add_argument("--view", type=int, default=0)
+    ap.add_argument("--tri-depth", type=int, default=0)
     a = ap.parse_args()
     t0 = time.time()
     sc = scenes.make_scene(a.config)
     gen = time.time() - t0
     cam = sc.cameras[a.view]
-    r = R.renderer_for(sc, max_pairs=24 << 20, sort_mode=a.sort_mode)
+    r = R.renderer_for(sc, max_pairs=24 << 20, sort_mode=a.sort_mode, tri_depth=a.tri_depth)
     ds = R.to_device(sc)
     out = torch.empty((cam.height, cam.width, 4), device="cuda")
     for _ in range(3):
