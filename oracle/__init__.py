@@ -19,15 +19,16 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "unimgs_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "bind_oracle.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared"]
 
 
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (no contraction, no fast-math, SSE2 scalar floats)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(s) for s in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, *_SRCS, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -104,6 +105,12 @@ def lib():
         L.or_rodrigues_public.restype = None
         L.or_tri_tile_depth.argtypes = [vp, i64, i32, i32]
         L.or_tri_tile_depth.restype = C.c_float
+        L.or_ray_cast.argtypes = [vp, vp, i64, vp, i64, vp, vp, vp, vp]
+        L.or_ray_cast.restype = i64
+        L.or_bind_targets.argtypes = [vp, vp, vp, i32, C.c_float, vp]
+        L.or_bind_targets.restype = None
+        L.or_bind.argtypes = [i64, vp, vp, vp, i64, vp, i64, vp, i32, vp, i32, C.c_float, vp, vp, vp, i32]
+        L.or_bind.restype = i32
         _lib = L
     return _lib
 
@@ -309,7 +316,8 @@ def coverage_mask(xy6, x: int, y: int) -> int:
 
 def rodrigues(w) -> np.ndarray:
     R = np.zeros(9, np.float64)
-    lib().or_rodrigues_public(_ptr(np.ascontiguousarray(w, np.float64)), _ptr(R))
+    w = np.ascontiguousarray(w, np.float64)  # keep the array alive across the call
+    lib().or_rodrigues_public(_ptr(w), _ptr(R))
     return R.reshape(3, 3)
 
 
@@ -332,3 +340,55 @@ def scene_settings(scene, **over):
              bg_alpha=float(scene.bg_alpha))
     s.update(over)
     return s
+
+
+# ---------------------------------------------------------------------------
+# Gaussian-centric ray-cast binding (oracle/bind_oracle.c, readings B1-B6)
+# ---------------------------------------------------------------------------
+
+def ray_cast(origin, direction, positions, faces):
+    """Nearest hit of one ray over all faces: (face or -1, t, u, v)."""
+    o = np.ascontiguousarray(origin, np.float64)
+    d = np.ascontiguousarray(direction, np.float64)
+    P = np.ascontiguousarray(positions, np.float32)
+    Fc = np.ascontiguousarray(faces, np.int32)
+    t, u, v = C.c_double(), C.c_double(), C.c_double()
+    f = lib().or_ray_cast(_ptr(o), _ptr(d), len(P), _ptr(P), len(Fc), _ptr(Fc), C.byref(t), C.byref(u), C.byref(v))
+    return int(f), t.value, u.value, v.value
+
+
+def bind_targets(mean, quat, scale, mode: int, k_sigma: float = 3.0) -> np.ndarray:
+    out = np.zeros((8, 3), np.float64)
+    m = np.ascontiguousarray(mean, np.float32)
+    q = np.ascontiguousarray(quat, np.float32)
+    s = np.ascontiguousarray(scale, np.float32)
+    lib().or_bind_targets(_ptr(m), _ptr(q), _ptr(s), mode, float(k_sigma), _ptr(out))
+    return out[:1] if mode == 0 else out
+
+
+def camera_array(cams) -> np.ndarray:
+    """[C, 12] float32: R (row-major, world->camera) then t."""
+    return np.ascontiguousarray(np.stack([np.concatenate([np.asarray(c.R, np.float32).ravel(),
+                                                          np.asarray(c.t, np.float32).ravel()]) for c in cams]),
+                                np.float32)
+
+
+def bind(gaussians, positions, faces, cams, mode: int = 1, k_sigma: float = 3.0, threads: int = 0):
+    """Exhaustive binding table: face [N, K] int32 (-1 = no hit), bary [N, K, 3] float64,
+    squared hit distance to the centre [N, K] (-1 = no hit); K = 1 (centre) or 8 (bbx8)."""
+    N = gaussians.count
+    K = 1 if mode == 0 else 8
+    mu = np.ascontiguousarray(gaussians.means, np.float32)
+    q = np.ascontiguousarray(gaussians.quats, np.float32)
+    s = np.ascontiguousarray(gaussians.scales, np.float32)
+    P = np.ascontiguousarray(positions, np.float32)
+    Fc = np.ascontiguousarray(faces, np.int32)
+    ca = camera_array(cams)
+    face = np.zeros((N, K), np.int32)
+    bary = np.zeros((N, K, 3), np.float64)
+    d2 = np.zeros((N, K), np.float64)
+    rc = lib().or_bind(N, _ptr(mu), _ptr(q), _ptr(s), len(P), _ptr(P), len(Fc), _ptr(Fc), len(ca), _ptr(ca), mode,
+                       float(k_sigma), _ptr(face), _ptr(bary), _ptr(d2), threads)
+    if rc:
+        raise ValueError("bind: need >= 1 camera and mode 0 or 1")
+    return face, bary, d2

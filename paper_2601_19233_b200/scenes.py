@@ -574,3 +574,29 @@ def make_deform(seed=6, n_gauss=20000, K=8, W=160, H=120, lon=48, lat=24):
     cam = look_at((0.0, 0.6, 3.4), width=W, height=H, fx=W * 0.9, fy=W * 0.9, cx=W / 2, cy=H / 2)
     binding = make_binding(rng, g, mesh, K)
     return Scene("deform", g, mesh, [cam], bg=np.array([0.1, 0.1, 0.1], np.float32)), binding
+
+
+# ----------------------------------------------------------------------------
+# ray-cast binding inputs: Gaussians on and
+# around a proxy-mesh shell seen by a ring of "training" cameras (SPEC's
+# workload: 100k Gaussians, bbx8, 8 cameras, 50k faces).
+# ----------------------------------------------------------------------------
+
+def make_bind_case(seed=8, n_gauss=100_000, lon=250, lat=100, n_cams=8, shell_sigma=0.01):
+    """(gaussians, mesh, cameras): UV sphere r = 1 with 2 lon lat faces, Gaussians at
+    radius ~ N(1, shell_sigma) with log-normal scales (median 0.01), cameras on an
+    orbit of radius 3 at alternating elevations looking at the origin."""
+    rng = np.random.default_rng(seed)
+    p, uv, f = uv_sphere((0, 0, 0), 1.0, lon, lat)
+    mesh = Mesh(p.astype(np.float32), f.astype(np.int32), np.ones(len(f), np.float32))
+    dirs = _unit_vectors(rng, n_gauss)
+    means = dirs * rng.normal(1.0, shell_sigma, (n_gauss, 1))
+    scales = _lognormal_scales(rng, n_gauss, 0.01, 0.5)
+    g = _pack_gaussians(means, _quats(rng, n_gauss), scales, _opacities(rng, n_gauss), _sh(rng, n_gauss, 0), 0)
+    cams = []
+    for i in range(n_cams):
+        phi = 2 * np.pi * i / n_cams
+        el = np.deg2rad(25.0 if i % 2 else -20.0)
+        eye = (3.0 * np.cos(el) * np.sin(phi), 3.0 * np.sin(el), 3.0 * np.cos(el) * np.cos(phi))
+        cams.append(look_at(eye, width=800, height=800, fx=900.0, fy=900.0, cx=400.0, cy=400.0))
+    return g, mesh, cams
