@@ -218,6 +218,36 @@ UNIMGS_API int unimgs_render(unimgs_ctx *c, float *out_rgbt, void *stream);
 UNIMGS_API int unimgs_deform(const unimgs_gaussians *rest, const unimgs_binding *binding,
                              const unimgs_vertex_field *field, float *means_out, float *cov_out, void *stream);
 
+/* Gaussian-centric ray-cast binding (§3.3.1; B1-B6).
+ * For every Gaussian and target -- its centre (mode 0, "UniMGS*") or the 8
+ * corners mu + R (+-k s0, +-k s1, +-k s2) of its oriented box at k = k_sigma
+ * standard deviations (mode 1, "UniMGS"; corner i takes + on axis a iff bit a
+ * of i is set) -- a ray is cast from each camera centre through the target
+ * (cameras that see the target at view z <= 0 are skipped).  Per ray the
+ * nearest Moller-Trumbore hit (|det| >= 1e-9, t > 1e-6; ties to the lower
+ * face id); per target the hit nearest the Gaussian centre over the cameras
+ * ("bound to the nearest candidate face"; ties: lower face id, then the
+ * earlier camera).  Arithmetic: IEEE double in a fixed order, so the table
+ * equals exhaustive search bit for bit.
+ *   g: count, means, quats, scales (device; quats/scales only for mode 1)
+ *   m: num_vertices, num_triangles, positions, faces (device; faces with an
+ *      out-of-range vertex id are ignored)
+ *   cams: HOST array of num_cams >= 1 cameras (only R and t are used)
+ *   face_out [N][K] int32 (-1 = no camera ray hit the mesh), bary_out
+ *   [N][K][3] float (weights of face vertices 0, 1, 2; zeros when unbound),
+ *   dist2_out [N][K] double squared hit distance to the centre (-1 unbound) or
+ *   NULL; K = 1 or 8.  Layout matches unimgs_binding for unimgs_deform.
+ * Builds an LBVH over the mesh in stream-ordered scratch (cudaMallocAsync,
+ * freed on the stream); asynchronous; not graph-capturable.  No context. */
+typedef struct {
+    int32_t mode;   /* 0 = centre, 1 = bbx8 */
+    float k_sigma;  /* box half-extent in standard deviations (> 0; 3 by convention) */
+} unimgs_bind_settings;
+
+UNIMGS_API int unimgs_bind(const unimgs_gaussians *g, const unimgs_mesh *m, const unimgs_camera *cams,
+                           int32_t num_cams, const unimgs_bind_settings *s, int32_t *face_out, float *bary_out,
+                           double *dist2_out, void *stream);
+
 /* Measurement variant of unimgs_render: identical output, plus the blend's
  * work counts (host work[4]): Gaussian entries tested, Gaussian fragments
  * blended, triangle entries tested, triangle fragments blended, summed over

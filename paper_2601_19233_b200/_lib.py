@@ -18,7 +18,11 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "UNSUPPORTED", 3: "CAPACITY",
 EXPORTS = ("unimgs_default_settings", "unimgs_create", "unimgs_set_settings", "unimgs_reserve", "unimgs_reserve2",
            "unimgs_preprocess", "unimgs_bin", "unimgs_render", "unimgs_render_counted", "unimgs_get_stats", "unimgs_get_bins",
            "unimgs_get_records", "unimgs_render_host", "unimgs_launch_count", "unimgs_error_string",
-           "unimgs_destroy", "unimgs_deform")
+           "unimgs_destroy", "unimgs_deform", "unimgs_bind")
+
+
+class BindSettings(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("k_sigma", C.c_float)]
 
 
 class Camera(C.Structure):
@@ -89,6 +93,9 @@ def load():
     L.unimgs_render_host.argtypes = [vp, C.POINTER(Gaussians), C.POINTER(Mesh), C.POINTER(Camera), i32, vp, vp]
     L.unimgs_deform.argtypes = [C.POINTER(Gaussians), C.POINTER(Binding), C.POINTER(VertexField), vp, vp, vp]
     L.unimgs_deform.restype = C.c_int
+    L.unimgs_bind.argtypes = [C.POINTER(Gaussians), C.POINTER(Mesh), C.POINTER(Camera), C.c_int32,
+                              C.POINTER(BindSettings), vp, vp, vp, vp]
+    L.unimgs_bind.restype = C.c_int
     L.unimgs_launch_count.argtypes = [vp]
     L.unimgs_launch_count.restype = i64
     L.unimgs_error_string.argtypes = [vp]

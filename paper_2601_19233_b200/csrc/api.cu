@@ -7,6 +7,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "../../include/unimgs.h"
 #include "internal.cuh"
@@ -317,6 +318,29 @@ extern "C" int unimgs_deform(const unimgs_gaussians *rest, const unimgs_binding 
     DeformInput d{rest->count, rest->means, rest->quats, rest->scales, rest->cov3d, b->anchors, b->face, b->bary,
                   f->num_faces, f->faces, reinterpret_cast<const float4 *>(f->data)};
     launch_deform(d, means_out, cov_out, (cudaStream_t)stream);
+    return cudaGetLastError() == cudaSuccess ? UNIMGS_OK : UNIMGS_ERR_CUDA;
+}
+
+extern "C" int unimgs_bind(const unimgs_gaussians *g, const unimgs_mesh *m, const unimgs_camera *cams, int32_t num_cams,
+                           const unimgs_bind_settings *s, int32_t *face_out, float *bary_out, double *dist2_out,
+                           void *stream) {
+    if (!g || !m || !cams || !s || !face_out || !bary_out || num_cams < 1 || g->count < 0 || m->num_triangles < 0 ||
+        m->num_vertices < 0)
+        return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (s->mode != 0 && s->mode != 1) return UNIMGS_ERR_UNSUPPORTED;
+    if (s->mode == 1 && !(s->k_sigma > 0.f && std::isfinite(s->k_sigma))) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (g->count > 0 && (!g->means || (s->mode == 1 && (!g->quats || !g->scales)))) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (m->num_triangles > 0 && (!m->positions || !m->faces)) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (m->num_triangles >= (1ll << 31) || g->count * (s->mode ? 8 : 1) >= (1ll << 40)) return UNIMGS_ERR_UNSUPPORTED;
+    std::vector<float> ca((size_t)num_cams * 12);
+    for (int i = 0; i < num_cams; i++) {
+        memcpy(&ca[12 * (size_t)i], cams[i].R, 9 * sizeof(float));
+        memcpy(&ca[12 * (size_t)i + 9], cams[i].t, 3 * sizeof(float));
+    }
+    if (g->count == 0) return UNIMGS_OK;
+    BindInput in{g->count, g->means, g->quats, g->scales, s->mode, s->k_sigma, num_cams, ca.data(),
+                 m->num_vertices, m->num_triangles, m->positions, m->faces};
+    if (launch_bind(in, face_out, bary_out, dist2_out, (cudaStream_t)stream) < 0) return UNIMGS_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? UNIMGS_OK : UNIMGS_ERR_CUDA;
 }
 

@@ -113,6 +113,18 @@ struct BlendParams {
     int msaa;   // M samples
 };
 
+struct BindInput {
+    int64_t N;
+    const float *means, *quats, *scales;  // device
+    int mode;                             // 0 = centre, 1 = bbx8
+    float k_sigma;
+    int ncams;
+    const float *cams;                    // HOST [ncams][12]: R row-major, then t
+    int64_t V, F;
+    const float *pos;                     // device [V][3]
+    const int32_t *faces;                 // device [F][3]
+};
+
 // ---- launchers (return number of kernels enqueued) --------------------------
 int launch_begin_frame(DevState *st, cudaStream_t s);
 int launch_preprocess_gaussians(const GaussInput &g, int64_t F, const CamParams &cam, float dilation,
@@ -125,6 +137,8 @@ int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, cons
                  const BlendParams &bp, float *out, cudaStream_t s, bool count_work = false);
 int launch_tile_stats(const Buffers &b, int tiles, cudaStream_t s);
 int launch_deform(const DeformInput &d, float *mu_out, float *cov_out, cudaStream_t s);
+// ray-cast binding (bind.cu): builds an LBVH in stream-ordered scratch; -1 if that allocation fails
+int launch_bind(const BindInput &in, int32_t *face_out, float *bary_out, double *dist2_out, cudaStream_t s);
 int launch_full_keys(const Buffers &b, uint64_t *keys, cudaStream_t s);
 
 }  // namespace unimgs

@@ -267,6 +267,32 @@ def deform(scene: DeviceScene, face: torch.Tensor, bary: torch.Tensor, faces: to
     return mo, co
 
 
+def bind(means: torch.Tensor, quats: torch.Tensor, scales: torch.Tensor, positions: torch.Tensor,
+         faces: torch.Tensor, cams, mode: int = 1, k_sigma: float = 3.0, with_dist: bool = False, stream=None):
+    """Gaussian-centric ray-cast binding on the device (unimgs_bind):
+    returns face [N,K] int32 (-1 = unbound), bary [N,K,3] float32 and, with
+    with_dist, the squared hit distance [N,K] float64; K = 1 (mode 0) or 8."""
+    L = _lib.load()
+    N = int(means.shape[0])
+    K = 1 if mode == 0 else 8
+    dev = means.device
+    g = _lib.Gaussians()
+    g.count, g.means, g.quats, g.scales = N, _ptr(means), _ptr(quats), _ptr(scales)
+    m = _lib.Mesh()
+    m.num_vertices, m.num_triangles = int(positions.shape[0]), int(faces.shape[0])
+    m.positions, m.faces = _ptr(positions), _ptr(faces)
+    ca = (_lib.Camera * len(cams))(*[c_camera(c) for c in cams])
+    s = _lib.BindSettings(mode, k_sigma)
+    face = torch.empty((N, K), dtype=torch.int32, device=dev)
+    bary = torch.empty((N, K, 3), dtype=torch.float32, device=dev)
+    d2 = torch.empty((N, K), dtype=torch.float64, device=dev) if with_dist else None
+    rc = L.unimgs_bind(C.byref(g), C.byref(m), ca, len(cams), C.byref(s), _ptr(face), _ptr(bary), _ptr(d2),
+                       _stream_handle(stream))
+    if rc != _lib.OK:
+        raise _lib.UnimgsError(rc, "bind")
+    return (face, bary, d2) if with_dist else (face, bary)
+
+
 def estimate_pairs(scene, slack: float = 2.0, minimum: int = 1 << 16) -> int:
     """A generous max_pairs for a scene (the caller may also size from get_stats)."""
     n = scene.gaussians.count + scene.mesh.num_triangles

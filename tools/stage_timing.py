@@ -48,7 +48,7 @@ def main():
         for i in range(3):
             acc[i] += ev[i].elapsed_time(ev[i + 1])
     ms = [x / a.iters for x in acc]
-    print(json.dumps(dict(config=a.config, sort_mode=a.sort_mode, gen_s=round(gen, 2), preprocess_ms=ms[0],
+    print(json.dumps(dict(config=a.config, sort_mode=a.sort_mode, tri_depth=a.tri_depth, gen_s=round(gen, 2), preprocess_ms=ms[0],
                           bin_ms=ms[1], render_ms=ms[2], frame_ms=sum(ms), fps=1000 / sum(ms), stats=st)))
 
 
