@@ -20,19 +20,22 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 from ncu_summary import raw, fnum  # noqa: E402
 
 
-def launch_shares(path, bench_views):
+def launch_shares(path):
+    """Per kernel name: launches, mean duration, and launches per frame (frames =
+    k_begin_frame launches; the warm-up, timed, isolated and counting passes of the
+    bench command all render whole frames, so per-frame averages are comparable)."""
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
-    launches = [(r[ki].split("(")[0].replace("void ", ""), float(r[vi].replace(",", ""))) for r in rows[hi + 1:]
-                if len(r) > vi]
-    # the timed region of the bench command is its last `bench_views` frames of 14 kernels
-    per_frame = collections.OrderedDict()
-    tail = launches[-bench_views * 14:]
-    for n, v in tail:
-        per_frame.setdefault(n, []).append(v)
-    return launches, per_frame
+    per = collections.OrderedDict()
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "").replace("unimgs::", "")
+        per.setdefault(name, []).append(float(r[vi].replace(",", "")))
+    frames = max(1, len(per.get("k_begin_frame", [])))
+    return per, frames
 
 
 def main():
@@ -41,19 +44,22 @@ def main():
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     shutil.copy(lpath, os.path.join(ROOT, "profiles", f"{tag}_launches.csv"))
     bench = json.load(open(bpath))
-    launches, per = launch_shares(lpath, 4)
-    tot = sum(sum(v) for v in per.values())
+    per, frames = launch_shares(lpath)
+    cmd = os.environ.get("PROFILE_CMD", "python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline")
+    frame_us = {k: sum(v) / frames for k, v in per.items()}
+    tot = sum(frame_us.values())
     lines = [f"# {tag}: ncu evidence for the bench line", ""]
     lines += ["## Bench line (bench.py, 1 GPU)", "", "```json", json.dumps(bench, indent=1)[:6000], "```", ""]
     if ref and os.path.exists(ref):
         lines += ["## Reference arm (CPU oracle)", "", "```json", open(ref).read().strip(), "```", ""]
     lines += ["## Launch list: kernel shares of a frame (ncu gpu__time_duration, cold-cache, serialised)", "",
-              "Command: `ncu --metrics gpu__time_duration.sum --clock-control none --csv "
-              "python bench.py --steps 2 --warmup 3 --views 2 --no-e2e --no-cpu-baseline` "
-              "(last 4 views = the timed region).", "",
-              "| kernel | launches | mean us | share of frame |", "|---|---|---|---|"]
+              f"Command: `ncu --metrics gpu__time_duration.sum --clock-control none --csv {cmd}`; "
+              f"{frames} frames (k_begin_frame launches) over the warm-up, timed, isolated-blend and "
+              "work-counting passes; `k_blend<1,...>` is the counting variant of the last pass.", "",
+              "| kernel | launches | mean us | us per frame | share of frame |", "|---|---|---|---|---|"]
     for k, v in per.items():
-        lines.append(f"| {k} | {len(v)} | {sum(v) / len(v) / 1e3:.1f} | {sum(v) / tot:.3f} |")
+        lines.append(f"| {k} | {len(v)} | {sum(v) / len(v) / 1e3:.1f} | {frame_us[k] / 1e3:.1f} | "
+                     f"{frame_us[k] / tot:.3f} |")
     lines.append("")
     rows = raw(rep)
     lines += ["## Full capture of one mip360 frame (`ncu --set full`)", "",
