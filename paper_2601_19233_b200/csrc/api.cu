@@ -131,7 +131,7 @@ extern "C" int unimgs_set_settings(unimgs_ctx *c, const unimgs_settings *s) {
 static void free_buffers(unimgs_ctx *c) {
     Buffers &b = c->buf;
     void *ptrs[] = {b.rect, b.touched, b.dkey, b.grec, b.trec, b.pk[0], b.pk[1], b.pv[0], b.pv[1], b.tk[0], b.tk[1],
-                    b.tv[0], b.tv[1], b.ranges, b.order, b.bcnt, b.dcnt, b.lookback, b.st};
+                    b.tv[0], b.tv[1], b.ranges, b.order, b.bcnt, b.dcnt, b.rstart, b.lookback, b.st};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     memset(&b, 0, sizeof b);
@@ -166,6 +166,7 @@ extern "C" int unimgs_reserve2(unimgs_ctx *c, int64_t max_gaussians, int64_t max
     CUDA_TRY(c, cudaMalloc(&b.order, sizeof(uint32_t) * tiles));
     CUDA_TRY(c, cudaMalloc(&b.bcnt, sizeof(uint32_t) * (size_t)(max_gaussians / 256 + max_triangles / 256 + 4)));
     CUDA_TRY(c, cudaMalloc(&b.dcnt, sizeof(uint32_t) * (size_t)(P / 2048 + 4)));
+    CUDA_TRY(c, cudaMalloc(&b.rstart, sizeof(uint32_t) * (size_t)(max_pairs / 1024 + 2)));
     CUDA_TRY(c, cudaMalloc(&b.lookback, sizeof(unsigned long long) * 256 * lb_tiles));
     CUDA_TRY(c, cudaMalloc(&b.st, sizeof(DevState)));
     CUDA_TRY(c, cudaMemset(b.lookback, 0, sizeof(unsigned long long) * 256 * lb_tiles));

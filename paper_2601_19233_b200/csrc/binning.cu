@@ -38,6 +38,9 @@
 #ifndef UNIMGS_SORT_ITEMS
 #define UNIMGS_SORT_ITEMS 16
 #endif
+#ifndef UNIMGS_DUP_EXPAND
+#define UNIMGS_DUP_EXPAND 1  // load-balanced pair expansion (k_expand) instead of k_duplicate
+#endif
 
 namespace unimgs {
 
@@ -181,31 +184,59 @@ __global__ void __launch_bounds__(256) k_compact(int64_t F, int64_t N, int nbt, 
     }
 }
 
+// Block-wide exclusive scan of warp-striped items (item i of lane l of warp w is
+// element w * 32 * ITEMS + i * 32 + l), saturating u32.
+template <int ITEMS>
+__device__ __forceinline__ void block_scan_striped(const unsigned (&val)[ITEMS], unsigned (&excl)[ITEMS],
+                                                   unsigned *s_w) {
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned carry = 0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        unsigned x = val[i];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (unsigned)o) x = sat_add(x, y);
+        }
+        const unsigned e = __shfl_up_sync(0xffffffffu, x, 1);
+        excl[i] = sat_add(carry, lane ? e : 0u);
+        carry = sat_add(carry, __shfl_sync(0xffffffffu, x, 31));
+    }
+    if (lane == 0) s_w[wid] = carry;
+    __syncthreads();
+    unsigned pre = 0;
+    for (unsigned w = 0; w < wid; w++) pre = sat_add(pre, s_w[w]);
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) excl[i] = sat_add(pre, excl[i]);
+}
+
 // Pair counts of CTA-sized runs (kScanTile) of the (sorted) visible primitives.
 __global__ void __launch_bounds__(kScanThreads) k_dup_count(const uint32_t *__restrict__ ids,
                                                             const uint32_t *__restrict__ touched, uint32_t *dcnt,
-                                                            const DevState *st) {
+                                                            uint32_t *prel, const DevState *st) {
     __shared__ unsigned s_w[8];
     const unsigned n = st->n_vis;
-    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
-    unsigned sum = 0;
-    if (base < n) {
-#pragma unroll
-        for (int i = 0; i < kScanItems; i++) {
-            const int64_t j = base + (int64_t)i * kScanThreads + threadIdx.x;
-            if (j < n) sum = sat_add(sum, touched[ids[j]]);
-        }
+    if (base >= n) {
+        if (threadIdx.x == 0) dcnt[blockIdx.x] = 0;
+        return;
     }
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int e0 = (int)wid * 32 * kScanItems + (int)lane;  // warp-striped element index
+    unsigned v[kScanItems], ex[kScanItems];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum = sat_add(sum, __shfl_xor_sync(0xffffffffu, sum, o));
-    if (lane == 0) s_w[wid] = sum;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned t = 0;
-        for (int w = 0; w < kScanThreads / 32; w++) t = sat_add(t, s_w[w]);
-        dcnt[blockIdx.x] = t;
+    for (int i = 0; i < kScanItems; i++) {
+        const int64_t j = base + e0 + 32 * i;
+        v[i] = j < n ? touched[ids[j]] : 0u;
     }
+    block_scan_striped<kScanItems>(v, ex, s_w);
+#pragma unroll
+    for (int i = 0; i < kScanItems; i++) {  // in-chunk exclusive prefix of each sorted position
+        const int64_t j = base + e0 + 32 * i;
+        if (j < n) prel[j] = ex[i];
+    }
+    if (threadIdx.x == kScanThreads - 1) dcnt[blockIdx.x] = sat_add(ex[kScanItems - 1], v[kScanItems - 1]);
 }
 
 // Depth-digit histograms (4 x 256 bins) of the compacted depth keys, for the
@@ -236,32 +267,6 @@ __global__ void __launch_bounds__(256) k_hist_depth(const uint32_t *__restrict__
     }
 }
 
-// Block-wide exclusive scan of warp-striped items (item i of lane l of warp w is
-// element w * 32 * ITEMS + i * 32 + l), saturating u32.
-template <int ITEMS>
-__device__ __forceinline__ void block_scan_striped(const unsigned (&val)[ITEMS], unsigned (&excl)[ITEMS],
-                                                   unsigned *s_w) {
-    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned carry = 0;
-#pragma unroll
-    for (int i = 0; i < ITEMS; i++) {
-        unsigned x = val[i];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= (unsigned)o) x = sat_add(x, y);
-        }
-        const unsigned e = __shfl_up_sync(0xffffffffu, x, 1);
-        excl[i] = sat_add(carry, lane ? e : 0u);
-        carry = sat_add(carry, __shfl_sync(0xffffffffu, x, 31));
-    }
-    if (lane == 0) s_w[wid] = carry;
-    __syncthreads();
-    unsigned pre = 0;
-    for (unsigned w = 0; w < wid; w++) pre = sat_add(pre, s_w[w]);
-#pragma unroll
-    for (int i = 0; i < ITEMS; i++) excl[i] = sat_add(pre, excl[i]);
-}
 
 // ----------------------------------------------------------------------------
 // k_duplicate: tiles_touched scan over the (depth-sorted or id-ordered) visible
@@ -405,6 +410,128 @@ __global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t *__re
         }
         __syncthreads();
     }
+    for (int i = threadIdx.x; i < 256; i += kScanThreads) {
+        if (s_hl[i]) atomicAdd(&st->hist[FULL ? 4 : HIST_TILE0][i], s_hl[i]);
+        if (s_hh[i]) atomicAdd(&st->hist[FULL ? 5 : HIST_TILE0 + 1][i], s_hh[i]);
+    }
+    if (FULL)
+        for (int i = threadIdx.x; i < 4 * 256; i += kScanThreads)
+            if (s_hd[FULL ? i : 0]) atomicAdd(&st->hist[i / 256][i % 256], s_hd[FULL ? i : 0]);
+}
+
+// ----------------------------------------------------------------------------
+// k_range_starts + k_expand: the same pairs as k_duplicate, load-balanced over
+// the OUTPUT.  The K pair slots are cut into ranges of ExpandCfg::SLOTS; the
+// global offset of sorted primitive i is dcnt[i / kScanTile] + prel[i] (the
+// chunk scan plus k_dup_count's in-chunk prefix), and k_range_starts records the
+// primitive holding the first slot of every range.  One CTA per range (grid-
+// stride) stages that range's primitives (<= SLOTS + 1: each has >= 1 pair) in
+// shared memory; each thread expands 8 consecutive slots after one binary search
+// (then walks forward), the keys and ids are staged and written out coalesced.
+// Slot order = (primitive order, tile row-major), as in k_duplicate.
+// ----------------------------------------------------------------------------
+template <bool FULL>
+struct ExpandCfg {
+    static constexpr int SLOTS = FULL ? 1024 : 2048;
+    static constexpr int PER = SLOTS / kScanThreads;  // slots per thread
+};
+
+__global__ void k_range_starts(const uint32_t *__restrict__ dcnt, const uint32_t *__restrict__ prel, int slots,
+                               uint32_t *rstart, const DevState *st) {
+    const unsigned n = st->n_vis, K = st->K;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned off = dcnt[i / kScanTile] + prel[i];
+        const unsigned nxt = i + 1 < n ? dcnt[(i + 1) / kScanTile] + prel[i + 1] : K;
+        for (unsigned r = (off + slots - 1) / slots; (unsigned long long)r * slots < nxt && r * slots < K; r++)
+            rstart[r] = i;
+    }
+}
+
+template <bool FULL>
+__global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restrict__ ids,
+                                                         const uint2 *__restrict__ rect,
+                                                         const uint32_t *__restrict__ dkey,
+                                                         const uint32_t *__restrict__ dcnt,
+                                                         const uint32_t *__restrict__ prel,
+                                                         const uint32_t *__restrict__ rstart, int tiles_x,
+                                                         const TriRecord *__restrict__ trec, unsigned F, int tri_depth,
+                                                         void *tk_, uint32_t *tv, DevState *st) {
+    using Key = typename DupCfg<FULL>::Key;
+    constexpr int SLOTS = ExpandCfg<FULL>::SLOTS, PER = ExpandCfg<FULL>::PER, MP = SLOTS + 2;
+    __shared__ int s_off[MP];          // primitive start slot relative to the range (first may be < 0)
+    __shared__ uint32_t s_id[MP];
+    __shared__ uint2 s_rect[MP];
+    __shared__ uint32_t s_dk[FULL ? MP : 1];
+    __shared__ Key s_k[SLOTS];
+    __shared__ uint32_t s_v[SLOTS];
+    __shared__ unsigned s_hl[256], s_hh[256];
+    __shared__ unsigned s_hd[FULL ? 4 * 256 : 1];
+    Key *tk = reinterpret_cast<Key *>(tk_);
+    if (st->overflow) return;
+    const unsigned K = st->K, n = st->n_vis;
+    const unsigned nranges = (K + SLOTS - 1) / SLOTS;
+    if (blockIdx.x >= nranges) return;
+    for (int i = threadIdx.x; i < 256; i += kScanThreads) s_hl[i] = s_hh[i] = 0;
+    if (FULL)
+        for (int i = threadIdx.x; i < 4 * 256; i += kScanThreads) s_hd[FULL ? i : 0] = 0;
+    for (unsigned r = blockIdx.x; r < nranges; r += gridDim.x) {
+        const unsigned S = r * SLOTS, E = min(K, S + SLOTS), ns = E - S;
+        const unsigned p0 = rstart[r];
+        const unsigned p1 = r + 1 < nranges ? rstart[r + 1] : n - 1;  // holds slot E (or E - 1)
+        const int m = (int)(p1 - p0) + 1;
+        __syncthreads();  // previous range's staging consumed
+        for (int j = threadIdx.x; j < m; j += kScanThreads) {
+            const unsigned i = p0 + j;
+            const uint32_t id = ids[i];
+            s_off[j] = (int)(dcnt[i / kScanTile] + prel[i]) - (int)S;
+            s_id[j] = id;
+            s_rect[j] = rect[id];
+            if (FULL) s_dk[FULL ? j : 0] = dkey[id];
+        }
+        if (threadIdx.x == 0) s_off[m] = 0x7FFFFFFF;  // sentinel for the forward walk
+        __syncthreads();
+        // thread t expands slots [t * PER, t * PER + PER) of the range
+        const int k0 = (int)threadIdx.x * PER;
+        if (k0 < (int)ns) {
+            int e = 0;  // largest e < m with s_off[e] <= k0
+            for (int step = 1 << (31 - __clz(m)); step >= 1; step >>= 1)
+                if (e + step < m && s_off[e + step] <= k0) e += step;
+            for (int q = 0; q < PER; q++) {
+                const int k = k0 + q;
+                if (k >= (int)ns) break;
+                while (s_off[e + 1] <= k) e++;
+                const uint2 rr = s_rect[e];
+                const unsigned x0 = rr.x & 0xFFFF, y0 = rr.x >> 16, x1 = rr.y & 0xFFFF;
+                const unsigned w = x1 - x0 + 1, local = (unsigned)(k - s_off[e]);
+                const unsigned qq = local / w;
+                const unsigned tx = x0 + (local - qq * w), ty = y0 + qq;
+                const unsigned t = ty * (unsigned)tiles_x + tx;
+                const uint32_t pid = s_id[e];
+                if (FULL) {
+                    uint32_t d = s_dk[FULL ? e : 0];
+                    if (tri_depth && pid < F) {  // N8 per-tile triangle depth
+                        const int4 *qp = reinterpret_cast<const int4 *>(trec + pid);
+                        d = tile_plane_depth_bits(__ldg(qp), __ldg(qp + 1),
+                                                  __ldg(reinterpret_cast<const float4 *>(qp + 2)), tx, ty);
+                    }
+                    s_k[k] = (Key)(((unsigned long long)t << 32) | d);
+#pragma unroll
+                    for (int dd = 0; dd < 4; dd++) atomicAdd(&s_hd[FULL ? dd * 256 + ((d >> (8 * dd)) & 255u) : 0], 1u);
+                } else {
+                    s_k[k] = (Key)t;
+                }
+                s_v[k] = pid;
+                atomicAdd(&s_hl[t & 255u], 1u);
+                atomicAdd(&s_hh[(t >> 8) & 255u], 1u);
+            }
+        }
+        __syncthreads();
+        for (unsigned k = threadIdx.x; k < ns; k += kScanThreads) {
+            tk[S + k] = s_k[k];
+            tv[S + k] = s_v[k];
+        }
+    }
+    __syncthreads();
     for (int i = threadIdx.x; i < 256; i += kScanThreads) {
         if (s_hl[i]) atomicAdd(&st->hist[FULL ? 4 : HIST_TILE0][i], s_hl[i]);
         if (s_hh[i]) atomicAdd(&st->hist[FULL ? 5 : HIST_TILE0 + 1][i], s_hh[i]);
@@ -760,14 +887,29 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         dup_ids = b.pv[0];
     }
     // pair counts per run of kScanTile primitives -> scan (K, capacity) -> emission
-    k_dup_count<<<dgrid, kScanThreads, 0, s>>>(dup_ids, b.touched, b.dcnt, b.st);
+    uint32_t *prel = b.pk[1];  // free after the depth sort (its result is in pk[0] / pv[0])
+    k_dup_count<<<dgrid, kScanThreads, 0, s>>>(dup_ids, b.touched, b.dcnt, prel, b.st);
     k_scan_counts<<<1, 1024, 0, s>>>(b.dcnt, dgrid, 1, b.max_pairs, b.st);
     launches += 2;
+#if UNIMGS_DUP_EXPAND
+    {
+        const int slots = full ? ExpandCfg<true>::SLOTS : ExpandCfg<false>::SLOTS;
+        k_range_starts<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, sm_count * 16)), 256, 0,
+                         s>>>(b.dcnt, prel, slots, b.rstart, b.st);
+        launches++;
+    }
+    const int egrid = (int)std::max<int64_t>(1, std::min<int64_t>((b.max_pairs + 1023) / 1024, sm_count * 4));
+#endif
     const int g2 = sort_grid(b.max_pairs, sm_count, 2);
     if (!full) {
+#if UNIMGS_DUP_EXPAND
+        k_expand<false><<<egrid, kScanThreads, 0, s>>>(dup_ids, b.rect, b.dkey, b.dcnt, prel, b.rstart, cam.tiles_x,
+                                                        b.trec, (unsigned)F, 0, b.tk[0], b.tv[0], b.st);
+#else
         k_duplicate<false><<<dgrid, kScanThreads, dup_smem<false>(), s>>>(dup_ids, b.touched, b.rect, b.dkey,
                                                                           cam.tiles_x, b.max_pairs, b.dcnt, b.trec,
                                                                           (unsigned)F, 0, b.tk[0], b.tv[0], b.st);
+#endif
         launches++;
         for (int pass = 0, sh = 0; sh < tb; pass++, sh += 8, slot++) {
             onesweep_pass<uint16_t>(b, (const uint16_t *)b.tk[tc], b.tv[tc], (uint16_t *)b.tk[tc ^ 1], b.tv[tc ^ 1],
@@ -779,9 +921,14 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         k_ranges16<<<sm_count * 4, 256, 0, s>>>((const uint16_t *)b.tk[tc], &b.st->K, b.ranges, b.st);
         launches++;
     } else {
+#if UNIMGS_DUP_EXPAND
+        k_expand<true><<<egrid, kScanThreads, 0, s>>>(dup_ids, b.rect, b.dkey, b.dcnt, prel, b.rstart, cam.tiles_x,
+                                                       b.trec, (unsigned)F, tri_depth, b.tk[0], b.tv[0], b.st);
+#else
         k_duplicate<true><<<dgrid, kScanThreads, dup_smem<true>(), s>>>(dup_ids, b.touched, b.rect, b.dkey, cam.tiles_x,
                                                                         b.max_pairs, b.dcnt, b.trec, (unsigned)F,
                                                                         tri_depth, b.tk[0], b.tv[0], b.st);
+#endif
         launches++;
         const int total_bits = 32 + tb;
         for (int pass = 0, sh = 0; sh < total_bits; pass++, sh += 8, slot++) {

@@ -72,6 +72,7 @@ struct Buffers {
     uint32_t *order;      // [tiles] blend schedule: tiles by decreasing pair count (approx., k_tile_order)
     uint32_t *bcnt;       // per-CTA visible counts of B2 then B1 (256 primitives each), scanned in place
     uint32_t *dcnt;       // per-CTA pair counts of the duplication (2048 primitives each), scanned in place
+    uint32_t *rstart;     // [max_pairs / 1024 + 2] first primitive of each expansion range (k_range_starts)
     unsigned long long *lookback;  // [max_lb_tiles][256]
     DevState *st;
     int64_t max_prims, max_pairs, max_tiles, max_lb_tiles;
