@@ -12,17 +12,19 @@
 //   sort_mode 0 (factored, default):
 //     k_onesweep<u32> x4   stable LSD on the 32-bit depth key of the visible
 //                          primitives (id ties stay in id order);
-//     k_dup_count + k_scan_counts + k_duplicate<false>   tiles_touched scan in
-//                          depth order (reduce-then-scan, sets K and the capacity
-//                          flag) and emission of (u16 tile, u32 id) pairs staged
-//                          through shared memory so every store is coalesced,
-//                          with the tile-digit histograms of the radix passes;
+//     k_dup_count + k_scan_counts + k_range_starts + k_expand<false>
+//                          tiles_touched scan in depth order (reduce-then-scan,
+//                          sets K and the capacity flag) and load-balanced
+//                          emission of (u16 tile, u32 id) pairs: fixed ranges of
+//                          output slots per CTA, staged so every store is
+//                          coalesced, with the tile-digit histograms of the
+//                          radix passes;
 //     k_onesweep<u16> x2   stable LSD on the tile id: pairs emitted in
 //                          (depth, id) order come out in (tile, depth, id)
 //                          order -- ~4x fewer bytes than sorting K 64-bit keys;
 //     k_ranges16           tile ranges from the sorted tile ids.
 //   sort_mode 1 (full, the literal form):
-//     k_duplicate<true>    (tile << 32 | depth, id) pairs in id order;
+//     k_expand<true>       (tile << 32 | depth, id) pairs in id order;
 //     k_onesweep<u64> x(4 + ceil(tile_bits/8)) over bits [0, 32 + tile_bits);
 //     k_ranges64.
 //
@@ -37,9 +39,6 @@
 
 #ifndef UNIMGS_SORT_ITEMS
 #define UNIMGS_SORT_ITEMS 16
-#endif
-#ifndef UNIMGS_DUP_EXPAND
-#define UNIMGS_DUP_EXPAND 1  // load-balanced pair expansion (k_expand) instead of k_duplicate
 #endif
 
 namespace unimgs {
@@ -94,7 +93,7 @@ __device__ __forceinline__ unsigned claim_tile(unsigned *ctr, unsigned *s_tile) 
 //   B1/B2 write one visible count per CTA of 256 primitives (bcnt);
 //   k_scan_counts scans a count array in place in one CTA;
 //   k_compact writes every visible primitive at its CTA offset + local rank;
-//   k_dup_count / k_scan_counts / k_duplicate do the same for the pairs.
+//   k_dup_count / k_scan_counts / k_expand do the same for the pairs.
 // ----------------------------------------------------------------------------
 // mode 0: total -> st->n_vis; mode 1: total -> needed / overflow / K (cap check)
 __global__ void __launch_bounds__(1024) k_scan_counts(uint32_t *cnt, int64_t n, int mode, int64_t cap, DevState *st) {
@@ -268,15 +267,9 @@ __global__ void __launch_bounds__(256) k_hist_depth(const uint32_t *__restrict__
 }
 
 
-// ----------------------------------------------------------------------------
-// k_duplicate: tiles_touched scan over the (depth-sorted or id-ordered) visible
-// primitives fused with the pair emission.  Each CTA's pairs form one
-// contiguous range; they are written into shared memory in windows of CAP pairs
-// by the owning threads, then copied out with coalesced stores.
-// ----------------------------------------------------------------------------
+// Pair key type: u16 tile id (sort_mode 0) or u64 (tile << 32 | depth bits).
 template <bool FULL>
 struct DupCfg {
-    static constexpr int CAP = FULL ? 4096 : 8192;
     using Key = typename std::conditional<FULL, unsigned long long, uint16_t>::type;
 };
 
@@ -300,127 +293,8 @@ __device__ __forceinline__ uint32_t tile_plane_depth_bits(const int4 q0, const i
     return __float_as_uint(fminf(fmaxf(__double2float_rn(__ddiv_rn((double)A2, s)), zmin), zmax));
 }
 
-template <bool FULL>
-__global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t *__restrict__ ids,
-                                                            const uint32_t *__restrict__ touched,
-                                                            const uint2 *__restrict__ rect,
-                                                            const uint32_t *__restrict__ dkey, int tiles_x,
-                                                            int64_t cap, const uint32_t *__restrict__ doff,
-                                                            const TriRecord *__restrict__ trec, unsigned F,
-                                                            int tri_depth, void *tk_, uint32_t *tv, DevState *st) {
-    using Key = typename DupCfg<FULL>::Key;
-    constexpr int CAP = DupCfg<FULL>::CAP;
-    extern __shared__ __align__(16) unsigned char smem[];
-    Key *s_k = reinterpret_cast<Key *>(smem);
-    uint32_t *s_v = reinterpret_cast<uint32_t *>(s_k + CAP);
-    __shared__ unsigned s_w[8], s_end;
-    __shared__ unsigned s_hl[256], s_hh[256];  // tile-digit histograms of this CTA's pairs
-    __shared__ unsigned s_hd[FULL ? 4 * 256 : 1];  // FULL: depth digits of the pair keys
-    Key *tk = reinterpret_cast<Key *>(tk_);
-    const int64_t n = (int64_t)st->n_vis;
-    const int64_t base = (int64_t)blockIdx.x * kScanTile;
-    if (base >= n || st->overflow) return;
-    const unsigned capu = (unsigned)(cap < 0xFFFFFFFFll ? cap : 0xFFFFFFFFll);
-    unsigned v[kScanItems], ex[kScanItems];
-    uint32_t id[kScanItems];
-    const int64_t b0 = base + (int64_t)(threadIdx.x >> 5) * 32 * kScanItems + (threadIdx.x & 31);  // warp-striped
-#pragma unroll
-    for (int i = 0; i < kScanItems; i++) {
-        const bool in = b0 + 32 * i < n;
-        id[i] = in ? ids[b0 + 32 * i] : 0u;
-        v[i] = in ? touched[id[i]] : 0u;
-    }
-    block_scan_striped<kScanItems>(v, ex, s_w);
-    const unsigned pbase = doff[blockIdx.x];
-#pragma unroll
-    for (int i = 0; i < kScanItems; i++) ex[i] = sat_add(ex[i], pbase);
-    if (threadIdx.x == kScanThreads - 1) s_end = sat_add(ex[kScanItems - 1], v[kScanItems - 1]);
-    uint2 r[kScanItems];
-    uint32_t dk[kScanItems];
-#pragma unroll
-    for (int i = 0; i < kScanItems; i++) {
-        r[i] = v[i] ? rect[id[i]] : make_uint2(0u, 0u);
-        dk[i] = (FULL && v[i]) ? dkey[id[i]] : 0u;
-    }
-    __syncthreads();
-    const unsigned pend = min(s_end, capu);
-    for (int i = threadIdx.x; i < 256; i += kScanThreads) s_hl[i] = s_hh[i] = 0;
-    if (FULL)
-        for (int i = threadIdx.x; i < 4 * 256; i += kScanThreads) s_hd[FULL ? i : 0] = 0;
-    for (unsigned wb = pbase; wb < pend; wb += CAP) {
-        const unsigned we = min(pend, wb + CAP);
-#pragma unroll
-        for (int i = 0; i < kScanItems; i++) {
-            if (!v[i]) continue;
-            const unsigned lo = max(ex[i], wb), hi = min(sat_add(ex[i], v[i]), we);
-            if (lo >= hi) continue;
-            const unsigned x0 = r[i].x & 0xFFFF, y0 = r[i].x >> 16, x1 = r[i].y & 0xFFFF;
-            const unsigned wdt = x1 - x0 + 1, l0 = lo - ex[i];
-            unsigned tx = x0 + l0 % wdt, ty = y0 + l0 / wdt;
-            const bool plane = FULL && tri_depth && id[i] < F;  // N8 per-tile triangle depth
-            int4 tq0 = make_int4(0, 0, 0, 0), tq1 = tq0;
-            float4 tq2 = make_float4(1.f, 1.f, 1.f, 1.f);
-            if (plane) {
-                const int4 *q = reinterpret_cast<const int4 *>(trec + id[i]);
-                tq0 = __ldg(q);
-                tq1 = __ldg(q + 1);
-                tq2 = __ldg(reinterpret_cast<const float4 *>(q + 2));
-            }
-            for (unsigned g = lo; g < hi; g++) {
-                const unsigned t = ty * (unsigned)tiles_x + tx;
-                if (FULL) {
-                    const uint32_t d = plane ? tile_plane_depth_bits(tq0, tq1, tq2, tx, ty) : dk[i];
-                    s_k[g - wb] = (Key)(((unsigned long long)t << 32) | d);
-                } else {
-                    s_k[g - wb] = (Key)t;
-                }
-                s_v[g - wb] = id[i];
-                if (++tx > x1) { tx = x0; ty++; }
-            }
-        }
-        __syncthreads();
-        for (unsigned k = threadIdx.x; k < we - wb; k += kScanThreads) {
-            tk[wb + k] = s_k[k];
-            tv[wb + k] = s_v[k];
-        }
-        // tile-digit histograms over contiguous segments of the window: the low
-        // digit of consecutive pairs varies (one atomic each, spread bins), the high
-        // digit runs (one atomic per run)
-        {
-            const unsigned nw = we - wb, seg = (nw + kScanThreads - 1) / kScanThreads;
-            const unsigned k0 = threadIdx.x * seg, k1 = min(nw, k0 + seg);
-            unsigned run_v = 0xFFFFFFFFu, run_n = 0;
-            for (unsigned k = k0; k < k1; k++) {
-                const unsigned t = FULL ? (unsigned)((unsigned long long)s_k[k] >> 32) : (unsigned)s_k[k];
-                atomicAdd(&s_hl[t & 255u], 1u);
-                if (FULL) {
-                    const unsigned long long kk = (unsigned long long)s_k[k];
-#pragma unroll
-                    for (int d = 0; d < 4; d++) atomicAdd(&s_hd[d * 256 + ((unsigned)(kk >> (8 * d)) & 255u)], 1u);
-                }
-                const unsigned h = (t >> 8) & 255u;
-                if (h != run_v) {
-                    if (run_n) atomicAdd(&s_hh[run_v], run_n);
-                    run_v = h;
-                    run_n = 0;
-                }
-                run_n++;
-            }
-            if (run_n) atomicAdd(&s_hh[run_v], run_n);
-        }
-        __syncthreads();
-    }
-    for (int i = threadIdx.x; i < 256; i += kScanThreads) {
-        if (s_hl[i]) atomicAdd(&st->hist[FULL ? 4 : HIST_TILE0][i], s_hl[i]);
-        if (s_hh[i]) atomicAdd(&st->hist[FULL ? 5 : HIST_TILE0 + 1][i], s_hh[i]);
-    }
-    if (FULL)
-        for (int i = threadIdx.x; i < 4 * 256; i += kScanThreads)
-            if (s_hd[FULL ? i : 0]) atomicAdd(&st->hist[i / 256][i % 256], s_hd[FULL ? i : 0]);
-}
-
 // ----------------------------------------------------------------------------
-// k_range_starts + k_expand: the same pairs as k_duplicate, load-balanced over
+// k_range_starts + k_expand: the (tile, primitive) pairs, load-balanced over
 // the OUTPUT.  The K pair slots are cut into ranges of ExpandCfg::SLOTS; the
 // global offset of sorted primitive i is dcnt[i / kScanTile] + prel[i] (the
 // chunk scan plus k_dup_count's in-chunk prefix), and k_range_starts records the
@@ -428,7 +302,7 @@ __global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t *__re
 // stride) stages that range's primitives (<= SLOTS + 1: each has >= 1 pair) in
 // shared memory; each thread expands 8 consecutive slots after one binary search
 // (then walks forward), the keys and ids are staged and written out coalesced.
-// Slot order = (primitive order, tile row-major), as in k_duplicate.
+// Slot order = (primitive order, tile row-major).
 // ----------------------------------------------------------------------------
 template <bool FULL>
 struct ExpandCfg {
@@ -775,10 +649,6 @@ static size_t onesweep_smem() {
 #endif
 constexpr int kDepthItems = UNIMGS_DEPTH_ITEMS;  // small depth sort: short tiles, latency-bound
 
-template <bool FULL>
-static size_t dup_smem() {
-    return DupCfg<FULL>::CAP * (sizeof(typename DupCfg<FULL>::Key) + sizeof(uint32_t));
-}
 
 static int bits_for(int64_t tiles) {
     int b = 0;
@@ -808,8 +678,6 @@ static void set_attrs() {
                          (int)onesweep_smem<uint32_t, kDepthItems>());
     cudaFuncSetAttribute(k_onesweep<unsigned long long, kSortItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)onesweep_smem<unsigned long long, kSortItems>());
-    cudaFuncSetAttribute(k_duplicate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dup_smem<false>());
-    cudaFuncSetAttribute(k_duplicate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dup_smem<true>());
     done = true;
 }
 
@@ -891,7 +759,6 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
     k_dup_count<<<dgrid, kScanThreads, 0, s>>>(dup_ids, b.touched, b.dcnt, prel, b.st);
     k_scan_counts<<<1, 1024, 0, s>>>(b.dcnt, dgrid, 1, b.max_pairs, b.st);
     launches += 2;
-#if UNIMGS_DUP_EXPAND
     {
         const int slots = full ? ExpandCfg<true>::SLOTS : ExpandCfg<false>::SLOTS;
         k_range_starts<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, sm_count * 16)), 256, 0,
@@ -899,17 +766,10 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         launches++;
     }
     const int egrid = (int)std::max<int64_t>(1, std::min<int64_t>((b.max_pairs + 1023) / 1024, sm_count * 4));
-#endif
     const int g2 = sort_grid(b.max_pairs, sm_count, 2);
     if (!full) {
-#if UNIMGS_DUP_EXPAND
         k_expand<false><<<egrid, kScanThreads, 0, s>>>(dup_ids, b.rect, b.dkey, b.dcnt, prel, b.rstart, cam.tiles_x,
                                                         b.trec, (unsigned)F, 0, b.tk[0], b.tv[0], b.st);
-#else
-        k_duplicate<false><<<dgrid, kScanThreads, dup_smem<false>(), s>>>(dup_ids, b.touched, b.rect, b.dkey,
-                                                                          cam.tiles_x, b.max_pairs, b.dcnt, b.trec,
-                                                                          (unsigned)F, 0, b.tk[0], b.tv[0], b.st);
-#endif
         launches++;
         for (int pass = 0, sh = 0; sh < tb; pass++, sh += 8, slot++) {
             onesweep_pass<uint16_t>(b, (const uint16_t *)b.tk[tc], b.tv[tc], (uint16_t *)b.tk[tc ^ 1], b.tv[tc ^ 1],
@@ -921,14 +781,8 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         k_ranges16<<<sm_count * 4, 256, 0, s>>>((const uint16_t *)b.tk[tc], &b.st->K, b.ranges, b.st);
         launches++;
     } else {
-#if UNIMGS_DUP_EXPAND
         k_expand<true><<<egrid, kScanThreads, 0, s>>>(dup_ids, b.rect, b.dkey, b.dcnt, prel, b.rstart, cam.tiles_x,
                                                        b.trec, (unsigned)F, tri_depth, b.tk[0], b.tv[0], b.st);
-#else
-        k_duplicate<true><<<dgrid, kScanThreads, dup_smem<true>(), s>>>(dup_ids, b.touched, b.rect, b.dkey, cam.tiles_x,
-                                                                        b.max_pairs, b.dcnt, b.trec, (unsigned)F,
-                                                                        tri_depth, b.tk[0], b.tv[0], b.st);
-#endif
         launches++;
         const int total_bits = 32 + tb;
         for (int pass = 0, sh = 0; sh < total_bits; pass++, sh += 8, slot++) {

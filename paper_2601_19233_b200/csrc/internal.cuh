@@ -25,8 +25,6 @@ struct DevState {
     unsigned int hist[kMaxPasses][256];
     unsigned int max_tile_pairs, max_tile_id;
     unsigned long long work[4];  // blend work counters (counting variant only)
-    unsigned int tdlo[257];      // difference array of the low tile-digit histogram
-    unsigned int tdlo_all;       // full 256-cycles of low tile digits
 };
 
 // Camera + the per-frame constants every stage needs.

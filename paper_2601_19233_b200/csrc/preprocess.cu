@@ -7,6 +7,10 @@
 // independent CPU oracle.  Colour (SH) is ordinary fp32.
 #include "internal.cuh"
 
+#ifndef UNIMGS_SH_PREFETCH
+#define UNIMGS_SH_PREFETCH 1
+#endif
+
 namespace unimgs {
 
 // explicit IEEE single ops: one rounding each, never contracted
@@ -129,6 +133,16 @@ __global__ void __launch_bounds__(256) k_preprocess_gaussians(GaussInput gin, in
             if (!(pv[2] > cam.near_z) || pv[2] > cam.far_z) break;
             const float xz = dv(pv[0], pv[2]), yz = dv(pv[1], pv[2]);          // N2
             const float u = fma_(cam.fx, xz, cam.cx), v = fma_(cam.fy, yz, cam.cy);
+#if UNIMGS_SH_PREFETCH
+            // likely visible: start pulling its SH coefficients into L2 now, so the
+            // EWA math below hides the latency of the dependent SH loads
+            if (u > -(float)cam.W && u < 2.f * (float)cam.W && v > -(float)cam.H && v < 2.f * (float)cam.H) {
+                const char *shp = reinterpret_cast<const char *>(gin.sh + g * (gin.sh_degree + 1) * (gin.sh_degree + 1) * 3);
+                const int bytes = (gin.sh_degree + 1) * (gin.sh_degree + 1) * 12;
+                for (int off = 0; off < bytes; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + off));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + bytes - 1));
+            }
+#endif
             float Sig[9];
             if (gin.cov3d) {  // given covariance (e.g. from the deformation transfer)
                 const float *cv = gin.cov3d + 6 * g;
