@@ -285,6 +285,29 @@ UNIMGS_API int unimgs_get_records(unimgs_ctx *c, float *grec, uint32_t *trec, ui
 UNIMGS_API int unimgs_render_host(unimgs_ctx *c, const unimgs_gaussians *g_host, const unimgs_mesh *m_host,
                        const unimgs_camera *cams, int32_t n_views, float *out_host, void *stream);
 
+/* Pipelined form of unimgs_render_host: enqueues the same work and returns
+ * without synchronising.  The context keeps two device copies of the scene,
+ * so the host->device upload of this call (on an internal copy stream) runs
+ * while the previous call still renders on `stream`, and the frame read-backs
+ * run on a third stream.  The host input arrays and out_host must stay valid
+ * and unmodified until unimgs_host_wait returns (or, for the inputs, until
+ * the call after next has been issued).  Capacity overflow is reported by
+ * unimgs_host_wait.  unimgs_render_host == render_host_async + host_wait. */
+UNIMGS_API int unimgs_render_host_async(unimgs_ctx *c, const unimgs_gaussians *g_host, const unimgs_mesh *m_host,
+                                        const unimgs_camera *cams, int32_t n_views, float *out_host, void *stream);
+
+/* Render lanes of the host path (1..8, default 1): lanes - 1 child contexts,
+ * each with the reserved scratch and its own stream, render the views of a
+ * unimgs_render_host[_async] call round-robin from the shared uploaded scene
+ * (independent views overlap one view's latency-bound binning with another's
+ * blend).  Must follow unimgs_reserve (re-call after growing); allocates and
+ * synchronises. */
+UNIMGS_API int unimgs_set_host_lanes(unimgs_ctx *c, int32_t lanes);
+
+/* Wait for every unimgs_render_host_async call of this context (uploads,
+ * renders, read-backs); UNIMGS_ERR_CAPACITY if the last frame overflowed. */
+UNIMGS_API int unimgs_host_wait(unimgs_ctx *c);
+
 /* Number of kernel launches enqueued by this context since creation. */
 UNIMGS_API int64_t unimgs_launch_count(const unimgs_ctx *c);
 

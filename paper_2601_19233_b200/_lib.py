@@ -18,7 +18,8 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "UNSUPPORTED", 3: "CAPACITY",
 EXPORTS = ("unimgs_default_settings", "unimgs_create", "unimgs_set_settings", "unimgs_reserve", "unimgs_reserve2",
            "unimgs_preprocess", "unimgs_bin", "unimgs_render", "unimgs_render_counted", "unimgs_get_stats", "unimgs_get_bins",
            "unimgs_get_records", "unimgs_render_host", "unimgs_launch_count", "unimgs_error_string",
-           "unimgs_destroy", "unimgs_deform", "unimgs_bind")
+           "unimgs_destroy", "unimgs_deform", "unimgs_bind", "unimgs_render_host_async", "unimgs_host_wait",
+           "unimgs_set_host_lanes")
 
 
 class BindSettings(C.Structure):
@@ -91,6 +92,12 @@ def load():
     L.unimgs_get_bins.argtypes = [vp, vp, vp, vp, vp]
     L.unimgs_get_records.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.unimgs_render_host.argtypes = [vp, C.POINTER(Gaussians), C.POINTER(Mesh), C.POINTER(Camera), i32, vp, vp]
+    L.unimgs_render_host_async.argtypes = [vp, C.POINTER(Gaussians), C.POINTER(Mesh), C.POINTER(Camera), i32, vp, vp]
+    L.unimgs_render_host_async.restype = C.c_int
+    L.unimgs_host_wait.argtypes = [vp]
+    L.unimgs_host_wait.restype = C.c_int
+    L.unimgs_set_host_lanes.argtypes = [vp, C.c_int32]
+    L.unimgs_set_host_lanes.restype = C.c_int
     L.unimgs_deform.argtypes = [C.POINTER(Gaussians), C.POINTER(Binding), C.POINTER(VertexField), vp, vp, vp]
     L.unimgs_deform.restype = C.c_int
     L.unimgs_bind.argtypes = [C.POINTER(Gaussians), C.POINTER(Mesh), C.POINTER(Camera), C.c_int32,

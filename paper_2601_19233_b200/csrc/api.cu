@@ -29,14 +29,27 @@ struct unimgs_ctx {
     int sm_count = 148;
     int64_t launches = 0;
     std::string err;
-    // end-to-end staging (unimgs_render_host)
-    void *stage_buf = nullptr;
-    size_t stage_bytes = 0;
+    // end-to-end staging (unimgs_render_host[_async]): two device copies of the
+    // scene, so the upload of call i + 1 overlaps the rendering of call i
+    void *stage_buf[2] = {nullptr, nullptr};
+    size_t stage_bytes[2] = {0, 0};
     float *frames[2] = {nullptr, nullptr};
     size_t frame_bytes = 0;
-    cudaStream_t copy_stream = nullptr;
+    cudaStream_t copy_stream = nullptr, up_stream = nullptr;
     cudaEvent_t ev_render[2] = {nullptr, nullptr}, ev_copy[2] = {nullptr, nullptr};
+    cudaEvent_t ev_uploaded[2] = {nullptr, nullptr}, ev_stage_free[2] = {nullptr, nullptr};
+    int64_t host_calls = 0;
+    cudaStream_t host_stream = nullptr;  // compute stream of the last async call
+    // extra render lanes of the host path (unimgs_set_host_lanes): child contexts with
+    // their own scratch, stream and frame buffers; views go round-robin over the lanes
+    static constexpr int kMaxLanes = 8;
+    int lanes = 1;
+    unimgs_ctx *child[kMaxLanes] = {};
+    cudaStream_t lane_stream[kMaxLanes] = {};
+    cudaEvent_t ev_lane_done[kMaxLanes] = {};
 };
+
+extern "C" void unimgs_destroy(unimgs_ctx *c);
 
 static int fail(unimgs_ctx *c, int code, const char *fmt, ...) __attribute__((format(printf, 3, 4)));
 static int fail(unimgs_ctx *c, int code, const char *fmt, ...) {
@@ -125,6 +138,10 @@ extern "C" int unimgs_set_settings(unimgs_ctx *c, const unimgs_settings *s) {
     if (rc) return rc;
     c->set = *s;
     c->stage = 0;
+    for (int l = 1; l < c->lanes; l++) {
+        c->child[l]->set = *s;
+        c->child[l]->stage = 0;
+    }
     return UNIMGS_OK;
 }
 
@@ -412,8 +429,8 @@ extern "C" int unimgs_get_records(unimgs_ctx *c, float *grec, uint32_t *trec, ui
 // ---- end-to-end path over host buffers ------------------------------------------
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-extern "C" int unimgs_render_host(unimgs_ctx *c, const unimgs_gaussians *gh, const unimgs_mesh *mh,
-                                  const unimgs_camera *cams, int32_t n_views, float *out_host, void *stream) {
+extern "C" int unimgs_render_host_async(unimgs_ctx *c, const unimgs_gaussians *gh, const unimgs_mesh *mh,
+                                        const unimgs_camera *cams, int32_t n_views, float *out_host, void *stream) {
     if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
     if (!c->reserved) return fail(c, UNIMGS_ERR_STATE, "render_host before reserve");
     if (!cams || n_views < 1 || !out_host) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "render_host: cams/out");
@@ -431,32 +448,46 @@ extern "C" int unimgs_render_host(unimgs_ctx *c, const unimgs_gaussians *gh, con
                          al256(tex ? (size_t)mh->tex_width * mh->tex_height * 4 : 0)};
     size_t total = 0;
     for (size_t x : sz) total += x;
-    if (total > c->stage_bytes) {
-        if (c->stage_buf) cudaFree(c->stage_buf);
-        c->stage_buf = nullptr;
-        c->stage_bytes = 0;
-        CUDA_TRY(c, cudaMalloc(&c->stage_buf, total));
-        c->stage_bytes = total;
-    }
-    const size_t fb = (size_t)W * H * 16;
-    if (fb > c->frame_bytes) {
-        for (int i = 0; i < 2; i++) {
-            if (c->frames[i]) cudaFree(c->frames[i]);
-            c->frames[i] = nullptr;
-        }
-        c->frame_bytes = 0;
-        for (int i = 0; i < 2; i++) CUDA_TRY(c, cudaMalloc(&c->frames[i], fb));
-        c->frame_bytes = fb;
-    }
+    cudaStream_t s = (cudaStream_t)stream;
     if (!c->copy_stream) {
         CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->up_stream, cudaStreamNonBlocking));
         for (int i = 0; i < 2; i++) {
             CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_render[i], cudaEventDisableTiming));
             CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming));
+            CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_uploaded[i], cudaEventDisableTiming));
+            CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_stage_free[i], cudaEventDisableTiming));
         }
     }
-    cudaStream_t s = (cudaStream_t)stream;
-    char *p = (char *)c->stage_buf;
+    const int slot = (int)(c->host_calls & 1);
+    if (total > c->stage_bytes[slot]) {  // growth: drain everything that may use the old buffer
+        CUDA_TRY(c, cudaDeviceSynchronize());
+        if (c->stage_buf[slot]) cudaFree(c->stage_buf[slot]);
+        c->stage_buf[slot] = nullptr;
+        c->stage_bytes[slot] = 0;
+        CUDA_TRY(c, cudaMalloc(&c->stage_buf[slot], total));
+        c->stage_bytes[slot] = total;
+    }
+    const size_t fb = (size_t)W * H * 16;
+    for (int l = 0; l < c->lanes; l++) {
+        unimgs_ctx *x = l ? c->child[l] : c;
+        if (fb > x->frame_bytes) {
+            CUDA_TRY(c, cudaDeviceSynchronize());
+            for (int i = 0; i < 2; i++) {
+                if (x->frames[i]) cudaFree(x->frames[i]);
+                x->frames[i] = nullptr;
+            }
+            x->frame_bytes = 0;
+            for (int i = 0; i < 2; i++) CUDA_TRY(c, cudaMalloc(&x->frames[i], fb));
+            x->frame_bytes = fb;
+        }
+        if (l && !x->ev_render[0])
+            for (int i = 0; i < 2; i++) {
+                CUDA_TRY(c, cudaEventCreateWithFlags(&x->ev_render[i], cudaEventDisableTiming));
+                CUDA_TRY(c, cudaEventCreateWithFlags(&x->ev_copy[i], cudaEventDisableTiming));
+            }
+    }
+    char *p = (char *)c->stage_buf[slot];
     char *dp[11];
     for (int i = 0; i < 11; i++) { dp[i] = p; p += sz[i]; }
     const void *src[] = {N ? gh->means : nullptr, N ? gh->quats : nullptr, N ? gh->scales : nullptr,
@@ -467,35 +498,106 @@ extern "C" int unimgs_render_host(unimgs_ctx *c, const unimgs_gaussians *gh, con
                             (size_t)V * 12, (mh && mh->uvs) ? (size_t)V * 8 : 0, (mh && mh->colors) ? (size_t)V * 12 : 0,
                             (size_t)F * 12, (size_t)F * 4,
                             tex ? (size_t)mh->tex_width * mh->tex_height * 4 : 0};
+    // upload on its own stream, once the call two back (same buffer) has rendered
+    if (c->host_calls >= 2) CUDA_TRY(c, cudaStreamWaitEvent(c->up_stream, c->ev_stage_free[slot], 0));
     for (int i = 0; i < 11; i++)
-        if (src[i] && bytes[i]) CUDA_TRY(c, cudaMemcpyAsync(dp[i], src[i], bytes[i], cudaMemcpyHostToDevice, s));
+        if (src[i] && bytes[i])
+            CUDA_TRY(c, cudaMemcpyAsync(dp[i], src[i], bytes[i], cudaMemcpyHostToDevice, c->up_stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev_uploaded[slot], c->up_stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_uploaded[slot], 0));
     unimgs_gaussians gd{N, (const float *)dp[0], (const float *)dp[1], (const float *)dp[2], (const float *)dp[3],
                         (const float *)dp[4], N ? gh->sh_degree : 0, nullptr};
     unimgs_mesh md{V, F, (const float *)dp[5], (F && mh->uvs) ? (const float *)dp[6] : nullptr,
                    (F && mh->colors) ? (const float *)dp[7] : nullptr, (const int32_t *)dp[8], (const float *)dp[9],
                    tex ? (const uint8_t *)dp[10] : nullptr, tex ? mh->tex_width : 0, tex ? mh->tex_height : 0};
+    for (int l = 1; l < c->lanes; l++) CUDA_TRY(c, cudaStreamWaitEvent(c->lane_stream[l], c->ev_uploaded[slot], 0));
     for (int v = 0; v < n_views; v++) {
-        const int bi = v & 1;
-        if (v >= 2) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_copy[bi], 0));
-        int rc = unimgs_preprocess(c, &gd, &md, &cams[v], stream);
-        if (!rc) rc = unimgs_bin(c, stream);
-        if (!rc) rc = unimgs_render(c, c->frames[bi], stream);
-        if (rc) return rc;
-        CUDA_TRY(c, cudaEventRecord(c->ev_render[bi], s));
-        CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_render[bi], 0));
-        CUDA_TRY(c, cudaMemcpyAsync(out_host + (size_t)v * W * H * 4, c->frames[bi], fb, cudaMemcpyDeviceToHost,
+        const int l = v % c->lanes;
+        unimgs_ctx *x = l ? c->child[l] : c;  // lane 0 is this context on the caller's stream
+        cudaStream_t ls = l ? c->lane_stream[l] : s;
+        const int bi = (v / c->lanes) & 1;
+        CUDA_TRY(c, cudaStreamWaitEvent(ls, x->ev_copy[bi], 0));  // frame buffer drained (no-op if never recorded)
+        int rc = unimgs_preprocess(x, &gd, &md, &cams[v], ls);
+        if (!rc) rc = unimgs_bin(x, ls);
+        if (!rc) rc = unimgs_render(x, x->frames[bi], ls);
+        if (rc) {
+            if (x != c) c->err = x->err;
+            return rc;
+        }
+        CUDA_TRY(c, cudaEventRecord(x->ev_render[bi], ls));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, x->ev_render[bi], 0));
+        CUDA_TRY(c, cudaMemcpyAsync(out_host + (size_t)v * W * H * 4, x->frames[bi], fb, cudaMemcpyDeviceToHost,
                                     c->copy_stream));
-        CUDA_TRY(c, cudaEventRecord(c->ev_copy[bi], c->copy_stream));
+        CUDA_TRY(c, cudaEventRecord(x->ev_copy[bi], c->copy_stream));
     }
-    CUDA_TRY(c, cudaStreamSynchronize(c->copy_stream));
-    CUDA_TRY(c, cudaStreamSynchronize(s));
-    DevState h;
-    CUDA_TRY(c, cudaMemcpy(&h, c->buf.st, sizeof h, cudaMemcpyDeviceToHost));
-    if (h.overflow) return fail(c, UNIMGS_ERR_CAPACITY, "capacity: %llu pairs needed", (unsigned long long)h.needed);
+    for (int l = 1; l < c->lanes; l++) {  // the scene slot is free once every lane has rendered
+        CUDA_TRY(c, cudaEventRecord(c->ev_lane_done[l], c->lane_stream[l]));
+        CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_lane_done[l], 0));
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev_stage_free[slot], s));
+    c->host_calls++;
+    c->host_stream = s;
     return UNIMGS_OK;
 }
 
-extern "C" int64_t unimgs_launch_count(const unimgs_ctx *c) { return c ? c->launches : 0; }
+extern "C" int unimgs_host_wait(unimgs_ctx *c) {
+    if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (!c->copy_stream) return UNIMGS_OK;
+    CUDA_TRY(c, cudaStreamSynchronize(c->up_stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->copy_stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->host_stream));
+    for (int l = 0; l < c->lanes; l++) {
+        unimgs_ctx *x = l ? c->child[l] : c;
+        if (l) CUDA_TRY(c, cudaStreamSynchronize(c->lane_stream[l]));
+        DevState h;
+        CUDA_TRY(c, cudaMemcpy(&h, x->buf.st, sizeof h, cudaMemcpyDeviceToHost));
+        if (h.overflow)
+            return fail(c, UNIMGS_ERR_CAPACITY, "capacity: %llu pairs needed", (unsigned long long)h.needed);
+    }
+    return UNIMGS_OK;
+}
+
+extern "C" int unimgs_set_host_lanes(unimgs_ctx *c, int32_t lanes) {
+    if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (!c->reserved) return fail(c, UNIMGS_ERR_STATE, "set_host_lanes before reserve");
+    if (lanes < 1 || lanes > unimgs_ctx::kMaxLanes)
+        return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "host lanes must be 1..%d", unimgs_ctx::kMaxLanes);
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    for (int l = 1; l < c->lanes; l++) {  // drop the previous lanes
+        unimgs_destroy(c->child[l]);
+        cudaStreamDestroy(c->lane_stream[l]);
+        cudaEventDestroy(c->ev_lane_done[l]);
+        c->child[l] = nullptr;
+    }
+    c->lanes = 1;
+    for (int l = 1; l < lanes; l++) {
+        int rc = unimgs_create(&c->child[l], &c->set);
+        if (!rc) rc = unimgs_reserve2(c->child[l], c->max_g, c->max_t, c->max_pairs, c->max_w, c->max_h);
+        if (rc) {
+            if (c->child[l]) unimgs_destroy(c->child[l]);
+            c->child[l] = nullptr;
+            return fail(c, rc, "set_host_lanes: lane %d allocation failed", l);
+        }
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->lane_stream[l], cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_lane_done[l], cudaEventDisableTiming));
+        c->lanes = l + 1;
+    }
+    return UNIMGS_OK;
+}
+
+extern "C" int unimgs_render_host(unimgs_ctx *c, const unimgs_gaussians *gh, const unimgs_mesh *mh,
+                                  const unimgs_camera *cams, int32_t n_views, float *out_host, void *stream) {
+    int rc = unimgs_render_host_async(c, gh, mh, cams, n_views, out_host, stream);
+    if (rc) return rc;
+    return unimgs_host_wait(c);
+}
+
+extern "C" int64_t unimgs_launch_count(const unimgs_ctx *c) {
+    if (!c) return 0;
+    int64_t n = c->launches;
+    for (int l = 1; l < c->lanes; l++) n += c->child[l]->launches;
+    return n;
+}
 
 extern "C" const char *unimgs_error_string(const unimgs_ctx *c) {
     if (!c) return "null context";
@@ -504,13 +606,23 @@ extern "C" const char *unimgs_error_string(const unimgs_ctx *c) {
 
 extern "C" void unimgs_destroy(unimgs_ctx *c) {
     if (!c) return;
+    for (int l = 1; l < c->lanes; l++) {
+        cudaStreamSynchronize(c->lane_stream[l]);
+        unimgs_destroy(c->child[l]);
+        cudaStreamDestroy(c->lane_stream[l]);
+        cudaEventDestroy(c->ev_lane_done[l]);
+    }
     free_buffers(c);
-    if (c->stage_buf) cudaFree(c->stage_buf);
+    if (c->copy_stream) cudaDeviceSynchronize();
     for (int i = 0; i < 2; i++) {
+        if (c->stage_buf[i]) cudaFree(c->stage_buf[i]);
         if (c->frames[i]) cudaFree(c->frames[i]);
         if (c->ev_render[i]) cudaEventDestroy(c->ev_render[i]);
         if (c->ev_copy[i]) cudaEventDestroy(c->ev_copy[i]);
+        if (c->ev_uploaded[i]) cudaEventDestroy(c->ev_uploaded[i]);
+        if (c->ev_stage_free[i]) cudaEventDestroy(c->ev_stage_free[i]);
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->up_stream) cudaStreamDestroy(c->up_stream);
     delete c;
 }

@@ -199,6 +199,26 @@ class Renderer:
                                               C.c_void_p(out.data_ptr()), _stream_handle(stream)))
         return out
 
+    def render_host_async(self, host_scene: DeviceScene, cams: Sequence[SceneCamera], out: torch.Tensor,
+                          stream=None):
+        """Pipelined render_host (unimgs_render_host_async): returns once enqueued; this call's
+        scene upload overlaps the previous call's rendering.  Keep host_scene, the camera list
+        and out alive until host_wait()."""
+        g, m = c_gaussians(host_scene), c_mesh(host_scene)
+        arr = (_lib.Camera * len(cams))(*[c_camera(c) for c in cams])
+        assert not out.is_cuda and out.is_contiguous()
+        self._keep = getattr(self, "_keep", [])[-3:] + [(g, m, arr)]  # ctypes structs stay referenced
+        self._check(self.L.unimgs_render_host_async(self._h, C.byref(g), C.byref(m), arr, len(cams),
+                                                    C.c_void_p(out.data_ptr()), _stream_handle(stream)))
+        return out
+
+    def host_wait(self):
+        self._check(self.L.unimgs_host_wait(self._h))
+
+    def set_host_lanes(self, lanes: int):
+        """Views of the host path render round-robin on `lanes` contexts/streams."""
+        self._check(self.L.unimgs_set_host_lanes(self._h, int(lanes)))
+
     # ---- stats / debug --------------------------------------------------------
     def stats(self, stream=None, check: bool = True) -> dict:
         st = _lib.Stats()

@@ -236,3 +236,33 @@ def test_fig3_overflow_on_gpu(built, oracle_mod):
         sel = (slice(14, 51), 32)
         ov[mode] = float(np.clip(img[sel][..., :3] - ss[sel][..., :3], 0, None).max())
     assert ov[0] < 0.02 and ov[3] >= 5 * ov[0] and ov[3] > 0.2, ov
+
+
+@pytest.mark.parametrize("lanes", [1, 3])
+def test_render_host_async_pipeline(built, lanes):
+    """Three overlapping pipelined calls (double-buffered device scene, views on 1 or 3
+    render lanes): every frame equals the device-resident render of its camera."""
+    import torch
+    from paper_2601_19233_b200 import renderer as R
+    sc = scenes.make_random(9, n_gauss=3000, n_tris=150)
+    cam0 = sc.cameras[0]
+    cams = []
+    for k in range(6):  # camera k: cam0 translated slightly
+        t = np.asarray(cam0.t, np.float32) + np.float32(0.02 * k)
+        cams.append(scenes.Camera(cam0.width, cam0.height, cam0.fx, cam0.fy, cam0.cx, cam0.cy, cam0.R, t))
+    r = R.renderer_for(sc)
+    ds = R.to_device(sc)
+    want = [r.render_view(ds, c).cpu() for c in cams]
+    host = R.to_pinned(sc)
+    r.set_host_lanes(lanes)
+    outs = [torch.full((2, cam0.height, cam0.width, 4), -1.0).pin_memory() for _ in range(3)]
+    for k in range(3):
+        r.render_host_async(host, cams[2 * k:2 * k + 2], outs[k])
+    r.host_wait()
+    for k in range(3):
+        for j in range(2):
+            assert torch.equal(outs[k][j], want[2 * k + j])
+    one = torch.empty((6, cam0.height, cam0.width, 4)).pin_memory()
+    r.render_host(host, cams, one)  # synchronous form, all six views over the lanes
+    for j in range(6):
+        assert torch.equal(one[j], want[j])
