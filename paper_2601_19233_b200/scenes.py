@@ -497,6 +497,63 @@ def make_crossing(W=128, H=96, n_gauss=0, alpha=1.0, seed=11) -> Scene:
     return Scene("crossing", g, mesh, [cam], bg=np.array([0.0, 0.0, 0.0], np.float32))
 
 
+def make_degenerate(seed=13, W=96, H=80):
+    """(scene_with_junk, base_scene): a valid random scene plus primitives the ABI
+    promises to cull as values (include/unimgs.h; N1-N7): NaN / inf means,
+    NaN and zero quaternions, inf scales, opacity 0, < 1/255 or NaN, a mean exactly
+    on the near plane or behind the camera; triangles with a NaN or inf vertex, a
+    vertex behind the near plane or beyond the 32768-px guard band, collinear
+    vertices, and out-of-range face indices.  Junk Gaussians are appended after the
+    valid ones and junk triangles after the valid triangles."""
+    base = make_random(seed, n_gauss=600, n_tris=40, W=W, H=H, textured=False, sh_degree=1)
+    g, m, cam = base.gaussians, base.mesh, base.cameras[0]
+    nan, inf = np.float32(np.nan), np.float32(np.inf)
+    R = np.asarray(cam.R, np.float64)
+    t = np.asarray(cam.t, np.float64)
+
+    def world(u, v, z):  # camera (u, v, z) -> world
+        pc = np.array([(u - cam.cx) / cam.fx * z, (v - cam.cy) / cam.fy * z, z])
+        return R.T @ (pc - t)
+
+    ok = world(W / 2, H / 2, 3.0)
+    jm, jq, js, jo = [], [], [], []
+
+    def add(mu, q=(1, 0, 0, 0), s=(0.05, 0.05, 0.05), o=0.8):
+        jm.append(mu); jq.append(q); js.append(s); jo.append(o)
+    add([nan, ok[1], ok[2]])
+    add([ok[0], ok[1], inf])
+    add(ok, q=(nan, 0, 0, 0))
+    add(ok, q=(0, 0, 0, 0))
+    add(ok, s=(inf, 0.05, 0.05))
+    add(ok, o=0.0)
+    add(ok, o=0.99 / 255.0)
+    add(ok, o=nan)
+    add(world(W / 2, H / 2, cam.near * (1 - 1e-4)))        # just in front of the near plane
+    add(world(W / 2, H / 2, -2.0))                         # behind the camera
+    k = g.sh.shape[1]
+    junk_g = Gaussians(np.asarray(jm, np.float32), np.asarray(jq, np.float32), np.asarray(js, np.float32),
+                       np.asarray(jo, np.float32), np.zeros((len(jm), k, 3), np.float32), g.sh_degree)
+    gall = Gaussians(np.concatenate([g.means, junk_g.means]), np.concatenate([g.quats, junk_g.quats]),
+                     np.concatenate([g.scales, junk_g.scales]), np.concatenate([g.opacities, junk_g.opacities]),
+                     np.concatenate([g.sh, junk_g.sh]), g.sh_degree)
+    V0 = m.num_vertices
+    a, b, c = world(20, 20, 2.0), world(60, 25, 2.5), world(30, 60, 2.2)
+    jp = [a, b, c,                                   # reused by the index-junk faces below
+          [nan, a[1], a[2]], b, c,                   # NaN vertex
+          [a[0], inf, a[2]], b, c,                   # inf vertex
+          world(20, 20, 0.1), b, c,                  # a vertex in front of the near plane
+          world(40000, 20, 3.0), b, c,               # beyond the guard band
+          world(20, 20, 2.0), world(40, 30, 2.0), world(60, 40, 2.0)]  # collinear on screen
+    jp = np.asarray(jp, np.float64)
+    jf = [[V0 + 3 * i, V0 + 3 * i + 1, V0 + 3 * i + 2] for i in range(1, 6)]
+    jf += [[V0, V0 + 1, -1], [V0, V0 + 1, V0 + len(jp) + 7]]  # out-of-range indices
+    pos = np.concatenate([m.positions, jp.astype(np.float32)])
+    faces = np.concatenate([m.faces, np.asarray(jf, np.int32)])
+    cols = np.concatenate([m.colors, np.full((len(jp), 3), 0.5, np.float32)])
+    mall = Mesh(pos, faces, np.concatenate([m.opacity, np.ones(len(jf), np.float32)]), colors=cols)
+    return Scene("degenerate", gall, mall, base.cameras, base.bg, base.bg_alpha), base
+
+
 # ----------------------------------------------------------------------------
 # deformation inputs (SURVEY §8(f) row 2; Eq.12-13, P:403-436): a bound proxy mesh
 # and a per-vertex transform field.  Synthetic: random nearby faces with Dirichlet

@@ -20,6 +20,7 @@ SMALL = {
     "nested": lambda: scenes.make_nested(),
     "edge": lambda: scenes.make_edge(),
     "overflow": lambda: scenes.make_overflow(),
+    "degenerate": lambda: scenes.make_degenerate()[0],
 }
 
 
@@ -266,3 +267,25 @@ def test_render_host_async_pipeline(built, lanes):
     r.render_host(host, cams, one)  # synchronous form, all six views over the lanes
     for j in range(6):
         assert torch.equal(one[j], want[j])
+
+
+def test_junk_is_invisible_on_gpu(built):
+    """NaN / inf / out-of-range primitives are culled as values on the GPU too: the
+    frame equals the frame of the valid scene alone; stats count only valid ones."""
+    import torch
+    from paper_2601_19233_b200 import renderer as R
+    sc, base = scenes.make_degenerate()
+    cam = sc.cameras[0]
+    r = R.renderer_for(sc)
+    img = r.render_view(R.to_device(sc), cam).clone()
+    st = r.stats()
+    rb = R.renderer_for(base)
+    ref = rb.render_view(R.to_device(base), cam).clone()
+    stb = rb.stats()
+    torch.cuda.synchronize()
+    assert torch.isfinite(img).all()
+    assert torch.equal(img, ref)
+    assert st["num_pairs"] == stb["num_pairs"]
+    assert st["visible_gaussians"] == stb["visible_gaussians"]
+    assert st["visible_triangles"] == stb["visible_triangles"]
+    assert st["culled_guard_band"] > stb["culled_guard_band"]
