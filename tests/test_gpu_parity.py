@@ -289,3 +289,41 @@ def test_junk_is_invisible_on_gpu(built):
     assert st["visible_gaussians"] == stb["visible_gaussians"]
     assert st["visible_triangles"] == stb["visible_triangles"]
     assert st["culled_guard_band"] > stb["culled_guard_band"]
+
+
+def test_multiview_bench_launch_configuration(built, oracle_mod):
+    """The bench's launch configuration at full size: 3M-Gaussian multiview scene,
+    views round-robin on 3 contexts / streams concurrently (bench.py step_fn).
+    Every frame equals the single-context render of its view bit for bit, and one
+    of them matches the oracle on sampled tiles."""
+    import torch
+    from paper_2601_19233_b200 import renderer as R
+    sc = scenes.make_multiview()
+    ds = R.to_device(sc)
+    cam0 = sc.cameras[0]
+    W, H = cam0.width, cam0.height
+    views = [3, 40, 77, 114, 151, 188]
+    nS = 3
+    rs = [R.Renderer(sc.gaussians.count, sc.mesh.num_triangles, 20 << 20, W, H,
+                     bg=tuple(float(v) for v in sc.bg), bg_alpha=float(sc.bg_alpha)) for _ in range(nS)]
+    streams = [torch.cuda.Stream() for _ in range(nS)]
+    out = torch.empty((len(views), H, W, 4), device="cuda")
+    s = torch.cuda.current_stream()
+    for st_ in streams:
+        st_.wait_stream(s)
+    for j, vi in enumerate(views):
+        rs[j % nS].render_view(ds, sc.cameras[vi], out=out[j], stream=streams[j % nS])
+    for st_ in streams:
+        s.wait_stream(st_)
+    torch.cuda.synchronize()
+    single = R.Renderer(sc.gaussians.count, sc.mesh.num_triangles, 20 << 20, W, H,
+                        bg=tuple(float(v) for v in sc.bg), bg_alpha=float(sc.bg_alpha))
+    for j, vi in enumerate(views):
+        ref = single.render_view(ds, sc.cameras[vi])
+        torch.cuda.synchronize()
+        assert torch.equal(out[j], ref), vi
+    o = oracle_mod.Oracle(sc.gaussians, sc.mesh)
+    o.project(sc.cameras[views[1]], **oracle_mod.scene_settings(sc))
+    o.bin()
+    tiles = np.random.default_rng(2).choice(o.tiles_x * o.tiles_y, 300, replace=False)
+    compare_image(out[1].cpu().numpy(), o.render(tiles))
