@@ -47,7 +47,7 @@ constexpr unsigned kFlagAgg = 1, kFlagInc = 2;
 constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
 constexpr int kSortThreads = 256, kSortItems = UNIMGS_SORT_ITEMS, kSortTile = kSortThreads * kSortItems;
 #ifndef UNIMGS_LOOKWIN
-#define UNIMGS_LOOKWIN 16
+#define UNIMGS_LOOKWIN 4
 #endif
 constexpr int kLookWin = UNIMGS_LOOKWIN;  // predecessors inspected per look-back round trip
 
