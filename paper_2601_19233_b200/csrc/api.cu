@@ -232,6 +232,8 @@ static int make_cam(unimgs_ctx *c, const unimgs_camera *cam, CamParams &cp) {
     for (int a = 0; a < 3; a++)
         cp.campos[a] = (float)(-((double)cam->R[a] * cam->t[0] + (double)cam->R[3 + a] * cam->t[1] +
                                  (double)cam->R[6 + a] * cam->t[2]));
+    if ((int64_t)cp.tiles_x * cp.tiles_y > (1ll << 24))
+        return fail(c, UNIMGS_ERR_UNSUPPORTED, "more than 2^24 tiles");  // three tile-digit histograms
     if ((int64_t)cp.tiles_x * cp.tiles_y > 65536 && c->set.sort_mode == 0 && c->set.tri_depth == 0)
         return fail(c, UNIMGS_ERR_UNSUPPORTED, "sort_mode 0 supports at most 65536 tiles; use sort_mode 1");
     return UNIMGS_OK;

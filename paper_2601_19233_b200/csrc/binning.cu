@@ -339,15 +339,20 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
     __shared__ Key s_k[SLOTS];
     __shared__ uint32_t s_v[SLOTS];
     __shared__ unsigned s_hl[256], s_hh[256];
+    __shared__ unsigned s_h3[FULL ? 256 : 1];  // mode 1: third tile digit (tile ids >= 65536)
     __shared__ unsigned s_hd[FULL ? 4 * 256 : 1];
     Key *tk = reinterpret_cast<Key *>(tk_);
     if (st->overflow) return;
     const unsigned K = st->K, n = st->n_vis;
     const unsigned nranges = (K + SLOTS - 1) / SLOTS;
     if (blockIdx.x >= nranges) return;
-    for (int i = threadIdx.x; i < 256; i += kScanThreads) s_hl[i] = s_hh[i] = 0;
+    for (int i = threadIdx.x; i < 256; i += kScanThreads) {
+        s_hl[i] = s_hh[i] = 0;
+        if (FULL) s_h3[FULL ? i : 0] = 0;
+    }
     if (FULL)
         for (int i = threadIdx.x; i < 4 * 256; i += kScanThreads) s_hd[FULL ? i : 0] = 0;
+    unsigned n_h3_zero = 0;
     for (unsigned r = blockIdx.x; r < nranges; r += gridDim.x) {
         const unsigned S = r * SLOTS, E = min(K, S + SLOTS), ns = E - S;
         const unsigned p0 = rstart[r];
@@ -397,6 +402,10 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
                 s_v[k] = pid;
                 atomicAdd(&s_hl[t & 255u], 1u);
                 atomicAdd(&s_hh[(t >> 8) & 255u], 1u);
+                if (FULL) {
+                    if (t >= 65536u) atomicAdd(&s_h3[FULL ? (t >> 16) & 255u : 0], 1u);
+                    else n_h3_zero++;  // third tile digit 0, added once per thread below
+                }
             }
         }
         __syncthreads();
@@ -405,10 +414,16 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
             tv[S + k] = s_v[k];
         }
     }
+    if (FULL && n_h3_zero) atomicAdd(&s_h3[0], n_h3_zero);
     __syncthreads();
     for (int i = threadIdx.x; i < 256; i += kScanThreads) {
         if (s_hl[i]) atomicAdd(&st->hist[FULL ? 4 : HIST_TILE0][i], s_hl[i]);
         if (s_hh[i]) atomicAdd(&st->hist[FULL ? 5 : HIST_TILE0 + 1][i], s_hh[i]);
+        // digit 0 of the third tile byte is every pair with a tile id < 65536
+        if (FULL) {
+            unsigned c3 = s_h3[FULL ? i : 0];
+            if (c3) atomicAdd(&st->hist[6][i], c3);
+        }
     }
     if (FULL)
         for (int i = threadIdx.x; i < 4 * 256; i += kScanThreads)

@@ -327,3 +327,26 @@ def test_multiview_bench_launch_configuration(built, oracle_mod):
     o.bin()
     tiles = np.random.default_rng(2).choice(o.tiles_x * o.tiles_y, 300, replace=False)
     compare_image(out[1].cpu().numpy(), o.render(tiles))
+
+
+def test_8k_image_full_keys(built, oracle_mod):
+    """7680x4320 = 129,600 tiles: more than the 16-bit tile keys of sort_mode 0 hold,
+    which is refused (UNSUPPORTED); sort_mode 1 (and tri_depth 1, which always uses
+    it) bins bit-exactly with 17-bit tile ids and renders within the tolerance."""
+    from paper_2601_19233_b200 import renderer as R, _lib
+    sc = scenes.make_random(21, n_gauss=2500, n_tris=300, W=7680, H=4320)
+    cam = sc.cameras[0]
+    r0 = R.renderer_for(sc, sort_mode=0)
+    with pytest.raises(_lib.UnimgsError) as e:
+        r0.preprocess(R.to_device(sc), cam)
+    assert e.value.code == _lib.ERR_UNSUPPORTED
+    for settings in ({"sort_mode": 1}, {"tri_depth": 1}):
+        r = R.renderer_for(sc, max_pairs=16 << 20, **settings)
+        img = r.render_view(R.to_device(sc), cam).cpu().numpy()
+        o = oracle_mod.Oracle(sc.gaussians, sc.mesh)
+        o.project(cam, **oracle_mod.scene_settings(sc, tri_depth=settings.get("tri_depth", 0)))
+        o.bin()
+        assert o.tiles_x * o.tiles_y > 65536
+        compare_bins(r, o)
+        tiles = np.random.default_rng(5).choice(o.tiles_x * o.tiles_y, 400, replace=False)
+        compare_image(img, o.render(tiles))
