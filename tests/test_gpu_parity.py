@@ -350,3 +350,15 @@ def test_8k_image_full_keys(built, oracle_mod):
         compare_bins(r, o)
         tiles = np.random.default_rng(5).choice(o.tiles_x * o.tiles_y, 400, replace=False)
         compare_image(img, o.render(tiles))
+
+
+@pytest.mark.parametrize("wh", [(1, 1), (17, 3), (16, 16)])
+@pytest.mark.parametrize("sort_mode", [0, 1])
+def test_tiny_images(built, oracle_mod, wh, sort_mode):
+    """One tile (zero tile-key bits: no tile passes), a ragged 2-tile strip, exactly one full tile."""
+    sc = scenes.make_random(30 + wh[0], n_gauss=300, n_tris=30, W=wh[0], H=wh[1])
+    cam = sc.cameras[0]
+    r, ds, img = run_gpu(sc, cam, sort_mode=sort_mode)
+    o = run_oracle(oracle_mod, sc, cam)
+    compare_bins(r, o)
+    compare_image(img, o.render())
