@@ -37,6 +37,9 @@
 
 #include "internal.cuh"
 
+#ifndef UNIMGS_SORT_PER_SM
+#define UNIMGS_SORT_PER_SM 2  // persistent sort-pass CTAs per SM
+#endif
 #ifndef UNIMGS_SORT_ITEMS
 #define UNIMGS_SORT_ITEMS 16
 #endif
@@ -757,7 +760,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         // depth sort of the visible primitives
         k_hist_depth<<<sm_count * 2, 256, 0, s>>>(b.pk[0], b.st);
         launches++;
-        const int g1 = sort_grid(P, sm_count, kDepthItems <= 4 ? 4 : 2, kSortThreads * kDepthItems);
+        const int g1 = sort_grid(P, sm_count, kDepthItems <= 4 ? 4 : UNIMGS_SORT_PER_SM, kSortThreads * kDepthItems);
         int cur = 0;
         for (int pass = 0; pass < 4; pass++, slot++) {
             onesweep_pass<uint32_t, kDepthItems>(b, b.pk[cur], b.pv[cur], b.pk[cur ^ 1], b.pv[cur ^ 1], &b.st->n_vis,
@@ -781,7 +784,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         launches++;
     }
     const int egrid = (int)std::max<int64_t>(1, std::min<int64_t>((b.max_pairs + 1023) / 1024, sm_count * 4));
-    const int g2 = sort_grid(b.max_pairs, sm_count, 2);
+    const int g2 = sort_grid(b.max_pairs, sm_count, UNIMGS_SORT_PER_SM);
     if (!full) {
         k_expand<false><<<egrid, kScanThreads, 0, s>>>(dup_ids, b.rect, b.dkey, b.dcnt, prel, b.rstart, cam.tiles_x,
                                                         b.trec, (unsigned)F, 0, b.tk[0], b.tv[0], b.st);
