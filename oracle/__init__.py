@@ -42,7 +42,7 @@ class CCamera(C.Structure):
 class CSettings(C.Structure):
     _fields_ = [("alpha_max", C.c_float), ("t_eps", C.c_float), ("dilation", C.c_float),
                 ("bg", C.c_float * 3), ("bg_alpha", C.c_float), ("blend_mode", C.c_int32), ("msaa", C.c_int32),
-                ("tri_depth", C.c_int32), ("tile_cull", C.c_int32)]
+                ("tri_depth", C.c_int32)]
 
 
 # blend modes: the paper's ablation (Fig.3 / Fig.4)
@@ -105,8 +105,6 @@ def lib():
         L.or_rodrigues_public.restype = None
         L.or_tri_tile_depth.argtypes = [vp, i64, i32, i32]
         L.or_tri_tile_depth.restype = C.c_float
-        L.or_gauss_row_span.argtypes = [vp, vp, i32, C.POINTER(C.c_int), C.POINTER(C.c_int)]
-        L.or_gauss_row_span.restype = None
         L.or_ray_cast.argtypes = [vp, vp, i64, vp, i64, vp, vp, vp, vp]
         L.or_ray_cast.restype = i64
         L.or_bind_targets.argtypes = [vp, vp, vp, i32, C.c_float, vp]
@@ -122,12 +120,11 @@ def _ptr(a: Optional[np.ndarray]):
 
 
 def make_settings(alpha_max=0.99, t_eps=1e-4, dilation=0.3, bg=(0.0, 0.0, 0.0), bg_alpha=1.0, blend_mode=EXACT,
-                  msaa=4, tri_depth=0, tile_cull=1) -> CSettings:
-    """tri_depth: 0 = centroid sort depth (R9), 1 = plane depth at the tile centre (N8).
-    tile_cull: 1 = per-row ellipse spans inside the N5 rect (N5'), 0 = the whole rect."""
+                  msaa=4, tri_depth=0) -> CSettings:
+    """tri_depth: 0 = centroid sort depth (R9), 1 = plane depth at the tile centre (N8)."""
     s = CSettings()
     s.alpha_max, s.t_eps, s.dilation, s.bg_alpha = alpha_max, t_eps, dilation, bg_alpha
-    s.blend_mode, s.msaa, s.tri_depth, s.tile_cull = blend_mode, msaa, tri_depth, tile_cull
+    s.blend_mode, s.msaa, s.tri_depth = blend_mode, msaa, tri_depth
     for i in range(3):
         s.bg[i] = float(bg[i])
     return s
@@ -234,15 +231,6 @@ class Oracle:
         lib().or_get_triangle_records(self._h, _ptr(out["xy"]), _ptr(out["vid"]), _ptr(out["z"]),
                                       _ptr(out["depth"]), _ptr(out["rect"]), _ptr(out["touched"]))
         return out
-
-    def gauss_row_span(self, g: int, ty: int):
-        """N5': [lo, hi] tile columns of rect row ty Gaussian g may cover (after project())."""
-        rec = self.gaussian_records()
-        r = np.ascontiguousarray(rec["rec"][g], np.float32)
-        rect = np.ascontiguousarray(rec["rect"][g], np.int32)
-        lo, hi = C.c_int(), C.c_int()
-        lib().or_gauss_row_span(_ptr(r), _ptr(rect), int(ty), C.byref(lo), C.byref(hi))
-        return lo.value, hi.value
 
     def tri_tile_depth(self, f: int, tx: int, ty: int) -> np.float32:
         """N8: sort depth of triangle f in tile (tx, ty) (after project())."""

@@ -54,7 +54,6 @@ typedef struct {
     int32_t blend_mode; /* OR_EXACT .. OR_PAPER_LITERAL */
     int32_t msaa;       /* M in {1, 2, 4, 8, 16} (P:330 uses 4) */
     int32_t tri_depth;  /* triangle sort depth: 0 = centroid (R9), 1 = plane depth at the tile centre (N8, NEXT 3) */
-    int32_t tile_cull;  /* Gaussian tiles: 0 = the whole N5 rect, 1 = per-row ellipse spans inside it (N5') */
 } or_settings;
 
 typedef struct {
@@ -181,52 +180,6 @@ static void sh_colour(const float *coef, int deg, const double dir[3], double ou
 void or_sh_basis_colour(const float *coef, int deg, const double *dir, double *out) { sh_colour(coef, deg, dir, out); }
 
 /* Gaussian projection, N1-N5 (EWA; 3DGS conventions S:161-169). */
-/* N5' (tile_cull = 1): the tiles of rect row ty that Gaussian g may
- * cover -- those whose pixel-centre box [16 tx + .5, 16 tx + 15.5] x [16 ty + .5,
- * 16 ty + 15.5] meets the padded ellipse {Q(d) <= q_max (1 + 2^-5)} of its fp32
- * conic.  The ellipse is convex, so per row they are one contiguous run [lo, hi]
- * of the rect's columns (lo > hi: none).  Its x-extent over the row band is
- * attained at a band end or at the ellipse's own x-extreme points
- * (dy = -/+ B xlim / C), computed in IEEE double in this order.  Conics with
- * (A + C)^2 > 1000 det keep the whole rect row (the pad covers the fp32 error of
- * N6 only for cond <~ 1000), so no tile with a fragment is ever dropped. */
-void or_gauss_row_span(const float *rec /* u v qmax o ka kb kc */, const int32_t *rect, int ty, int *lo, int *hi) {
-    const int x0 = rect[0], x1 = rect[2];
-    *lo = x0;
-    *hi = x1;
-    const double A = rec[4], B = rec[5], C = rec[6], Q = (double)rec[2] * 1.03125;
-    const double det = A * C - B * B;
-    if (!(det > 0.0) || !((A + C) * (A + C) <= 1000.0 * det)) return;
-    const double ylim = sqrt(Q * A / det), xlim = sqrt(Q * C / det);
-    double ya = ((double)(16 * ty) + 0.5) - (double)rec[1], yb = ((double)(16 * ty) + 15.5) - (double)rec[1];
-    if (ya < -ylim) ya = -ylim;
-    if (yb > ylim) yb = ylim;
-    if (!(ya <= yb)) { *lo = 1; *hi = 0; return; }
-    double ra = Q * A - det * ya * ya, rb = Q * A - det * yb * yb;
-    if (ra < 0.0) ra = 0.0;
-    if (rb < 0.0) rb = 0.0;
-    const double sa = sqrt(ra), sb = sqrt(rb);
-    const double dyr = -B * xlim / C, dyl = B * xlim / C;
-    double xr, xl;
-    if (ya <= dyr && dyr <= yb) {
-        xr = xlim;
-    } else {
-        const double r1 = (-B * ya + sa) / A, r2 = (-B * yb + sb) / A;
-        xr = r1 > r2 ? r1 : r2;
-    }
-    if (ya <= dyl && dyl <= yb) {
-        xl = -xlim;
-    } else {
-        const double l1 = (-B * ya - sa) / A, l2 = (-B * yb - sb) / A;
-        xl = l1 < l2 ? l1 : l2;
-    }
-    const double lo_d = ceil((((double)rec[0] + xl) - 15.5) / 16.0);
-    const double hi_d = floor((((double)rec[0] + xr) - 0.5) / 16.0);
-    if (!(lo_d <= (double)x1) || !(hi_d >= (double)x0) || !(lo_d <= hi_d)) { *lo = 1; *hi = 0; return; }
-    *lo = lo_d > (double)x0 ? (int)lo_d : x0;
-    *hi = hi_d < (double)x1 ? (int)hi_d : x1;
-}
-
 static void project_gaussian(or_ctx *c, int64_t i) {
     const or_camera *cam = &c->cam;
     float *rec = c->g_rec + 8 * i;
@@ -320,23 +273,7 @@ static void project_gaussian(or_ctx *c, int64_t i) {
     rec[4] = ka; rec[5] = kb; rec[6] = kc; rec[7] = pv[2];
     c->g_cov[3 * i + 0] = ca_; c->g_cov[3 * i + 1] = cb_; c->g_cov[3 * i + 2] = cc_;
     rect[0] = x0; rect[1] = y0; rect[2] = x1; rect[3] = y1;
-    if (c->set.tile_cull == 1) {  /* N5': count the per-row ellipse spans */
-        uint32_t n = 0;
-        for (int ty = y0; ty <= y1; ty++) {
-            int lo, hi;
-            or_gauss_row_span(rec, rect, ty, &lo, &hi);
-            if (lo <= hi) n += (uint32_t)(hi - lo + 1);
-        }
-        if (n == 0) {  /* no tile can hold a fragment: culled */
-            rect[0] = rect[1] = rect[2] = rect[3] = -1;
-            memset(rec, 0, 8 * sizeof(float));
-            memset(c->g_cov + 3 * i, 0, 3 * sizeof(float));
-            return;
-        }
-        c->g_touched[i] = n;
-    } else {
-        c->g_touched[i] = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
-    }
+    c->g_touched[i] = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
 
     /* colour: SH at dir = normalize(mu - campos), campos = -R^T t (double) */
     double cp[3], d[3], nrm = 0.0;
@@ -508,17 +445,14 @@ int64_t or_bin(or_ctx *c) {
         uint32_t touched = p < F ? c->t_touched[p] : c->g_touched[p - F];
         if (!touched) continue;
         const uint32_t db = f32_bits(prim_depth(c, (uint32_t)p));
-        for (int ty = rect[1]; ty <= rect[3]; ty++) {
-            int lo = rect[0], hi = rect[2];
-            if (p >= F && c->set.tile_cull == 1) or_gauss_row_span(c->g_rec + 8 * (p - F), rect, ty, &lo, &hi);
-            for (int tx = lo; tx <= hi; tx++) {
+        for (int ty = rect[1]; ty <= rect[3]; ty++)
+            for (int tx = rect[0]; tx <= rect[2]; tx++) {
                 uint64_t tile = (uint64_t)ty * (uint64_t)c->tiles_x + (uint64_t)tx;
                 const uint32_t d = p < F ? f32_bits(tri_key_depth(c, p, tx, ty)) : db;
                 pairs[n].key = (tile << 32) | d;
                 pairs[n].val = (uint32_t)p;
                 n++;
             }
-        }
     }
     qsort(pairs, (size_t)n, sizeof(or_pair), pair_cmp);
     int64_t T = (int64_t)c->tiles_x * c->tiles_y;
