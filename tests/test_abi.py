@@ -29,24 +29,30 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_struct_layouts_match_header():
-    """ctypes mirrors of the ABI structs have the sizes a C compiler gives them."""
+    """Every ctypes mirror of an ABI struct has the size and the field offsets a C
+    compiler gives the header's struct (catches drift between include/unimgs.h and
+    the Python binding)."""
     import subprocess
     import tempfile
     from paper_2601_19233_b200 import _lib
-    code = r'''
-#include <stdio.h>
-#include "unimgs.h"
-int main(void){printf("%zu %zu %zu %zu %zu\n", sizeof(unimgs_camera), sizeof(unimgs_gaussians),
- sizeof(unimgs_mesh), sizeof(unimgs_settings), sizeof(unimgs_stats)); return 0;}
-'''
+    pairs = [("unimgs_camera", _lib.Camera), ("unimgs_gaussians", _lib.Gaussians), ("unimgs_binding", _lib.Binding),
+             ("unimgs_vertex_field", _lib.VertexField), ("unimgs_mesh", _lib.Mesh), ("unimgs_settings", _lib.Settings),
+             ("unimgs_stats", _lib.Stats), ("unimgs_bind_settings", _lib.BindSettings)]
+    lines, want = [], []
+    for cname, py in pairs:
+        lines.append(f'printf("%zu\\n", sizeof({cname}));')
+        want.append(ctypes.sizeof(py))
+        for fname, _ in py._fields_:
+            lines.append(f'printf("%zu\\n", offsetof({cname}, {fname}));')
+            want.append(getattr(py, fname).offset)
+    code = "#include <stdio.h>\n#include <stddef.h>\n#include \"unimgs.h\"\nint main(void){" + "".join(lines) + "return 0;}"
     with tempfile.TemporaryDirectory() as d:
         c = os.path.join(d, "t.c")
         open(c, "w").write(code)
         exe = os.path.join(d, "t")
         subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
-        sizes = list(map(int, subprocess.check_output([exe]).split()))
-    mine = [ctypes.sizeof(x) for x in (_lib.Camera, _lib.Gaussians, _lib.Mesh, _lib.Settings, _lib.Stats)]
-    assert sizes == mine
+        got = list(map(int, subprocess.check_output([exe]).split()))
+    assert got == want
 
 
 def test_no_device_calls_fail_cleanly_without_gpu():
