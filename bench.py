@@ -361,11 +361,13 @@ def run_ours(a, rank, world, local_rank):
     sm_count = props.multi_processor_count
     peak_tops = sm_count * 128 * 1.965e9 / 1e12  # 4 schedulers x 32 lanes x max clock
     achieved = ops / (blend_max / 1000.0) / 1e12
-    traffic = None
+    traffic, ncu_issue = None, None
     tp = os.path.join(ROOT, "profiles", "blend_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            bt = json.load(open(tp))
+            traffic = bt.get("dram_bytes_per_launch")
+            ncu_issue = {k: bt.get(k) for k in ("issue_active_pct", "sm_active_frac", "issue_elapsed_pct")}
         except Exception:
             traffic = None
     peaks = {}
@@ -393,6 +395,7 @@ def run_ours(a, rank, world, local_rank):
                      "fragment_ops_per_launch": frag_ops,
                      "fragments_only_isolated_frac": frag_ops / (blend_iso_ms / 1000.0) / 1e12 / peak_tops,
                      "work_note": "ops = pixel-entry tests x test ops + fragments x blend ops (DESIGN.md §5)",
+                     "ncu_issue": ncu_issue,
                      "timing_note": f"avg_launch_ms from CUDA events on the launching streams inside the timed "
                                     f"region ({nS} overlapped streams); isolated_* from a single-stream pass",
                      "peak_note": f"{sm_count} SMs x 4 schedulers x 32 lanes x 1965 MHz (issue-slot lane-ops)",

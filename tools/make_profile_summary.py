@@ -74,7 +74,12 @@ def main():
                      f"{d['sm__warps_active.avg.pct_of_peak_sustained_active']} | "
                      f"{d['sm__inst_issued.avg.pct_of_peak_sustained_active']} | {d['launch__registers_per_thread']} |")
         if name.startswith("unimgs::k_blend") or name.startswith("k_blend"):
+            issue_active = fnum(d["sm__inst_issued.avg.pct_of_peak_sustained_active"])
+            cyc_act, cyc_el = fnum(d.get("smsp__cycles_active.avg", "nan")), fnum(d.get("sm__cycles_elapsed.avg", "nan"))
             blend = {"kernel": name, "dram_bytes_per_launch": mb * 1e6, "duration_us_ncu": t,
+                     "issue_active_pct": issue_active,
+                     "sm_active_frac": cyc_act / cyc_el if cyc_el == cyc_el and cyc_el > 0 else None,
+                     "issue_elapsed_pct": issue_active * cyc_act / cyc_el if cyc_el == cyc_el and cyc_el > 0 else None,
                      "source": f"profiles/{tag}_ncu_full.csv"}
     lines.append("")
     lines.append("DRAM MB are ncu's `dram__bytes_read.sum + dram__bytes_write.sum` (units as reported: MB).")

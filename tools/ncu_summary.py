@@ -9,7 +9,7 @@ import json
 import subprocess
 import sys
 
-METRICS = [
+METRICS = ["smsp__cycles_active.avg", "sm__cycles_elapsed.avg", 
     "gpu__time_duration.sum",
     "dram__bytes_read.sum",
     "dram__bytes_write.sum",
