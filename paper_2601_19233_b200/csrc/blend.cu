@@ -90,29 +90,33 @@ __device__ __forceinline__ unsigned coverage(const int X[3], const int Y[3], int
     return m;
 }
 
+// Colour of a covered triangle at the pixel centre (R12): perspective-correct,
+// unclamped barycentrics from the exact centre edge functions, in fp32 (colour
+// only has to meet the 1e-3 tolerance; w_k = E_k z_i z_j has ~6e-8 relative
+// error, far below it), bilinear texture in fp32.
 __device__ __forceinline__ void tri_colour(const TriRecord &r, const long long Ec[3], const TexView &tv, float rgb[3]) {
-    const double z0 = r.q2.x, z1 = r.q2.y, z2 = r.q2.z;
-    // w_k = b_k / z_k  ~  E_k * (product of the other two z): exact products in fp64
-    const double w0 = (double)Ec[0] * (z1 * z2), w1 = (double)Ec[1] * (z0 * z2), w2 = (double)Ec[2] * (z0 * z1);
-    const double sw = w0 + w1 + w2;
-    double l0, l1, l2;
-    if (sw != 0.0) {
-        const double is = 1.0 / sw;
+    const float z0 = r.q2.x, z1 = r.q2.y, z2 = r.q2.z;
+    // w_k = b_k / z_k  ~  E_k * (product of the other two z)
+    const float w0 = (float)Ec[0] * (z1 * z2), w1 = (float)Ec[1] * (z0 * z2), w2 = (float)Ec[2] * (z0 * z1);
+    const float sw = w0 + w1 + w2;
+    float l0, l1, l2;
+    if (sw != 0.0f) {
+        const float is = 1.0f / sw;
         l0 = w0 * is; l1 = w1 * is; l2 = w2 * is;
     } else {
-        const double A2 = (double)(Ec[0] + Ec[1] + Ec[2]);
-        l0 = Ec[0] / A2; l1 = Ec[1] / A2; l2 = Ec[2] / A2;
+        const float iA = 1.0f / (float)(Ec[0] + Ec[1] + Ec[2]);
+        l0 = (float)Ec[0] * iA; l1 = (float)Ec[1] * iA; l2 = (float)Ec[2] * iA;
     }
     const int kind = r.q1.z;
     if (kind == 1) {
-        const double uu = l0 * r.q3.x + l1 * r.q3.w + l2 * r.q4.z;
-        const double vv = l0 * r.q3.y + l1 * r.q4.x + l2 * r.q4.w;
-        const double txd = uu * tv.w - 0.5, tyd = vv * tv.h - 0.5;
-        const double fi = floor(txd), fj = floor(tyd);
-        const float ax = (float)(txd - fi), ay = (float)(tyd - fj);
+        const float uu = l0 * r.q3.x + l1 * r.q3.w + l2 * r.q4.z;
+        const float vv = l0 * r.q3.y + l1 * r.q4.x + l2 * r.q4.w;
+        const float txd = uu * (float)tv.w - 0.5f, tyd = vv * (float)tv.h - 0.5f;
+        const float fi = floorf(txd), fj = floorf(tyd);
+        const float ax = txd - fi, ay = tyd - fj;
         // clamp before converting so huge coordinates stay defined
-        const int i0 = (int)fmin(fmax(fi, -2.0), (double)tv.w + 1.0);
-        const int j0 = (int)fmin(fmax(fj, -2.0), (double)tv.h + 1.0);
+        const int i0 = (int)fminf(fmaxf(fi, -2.0f), (float)tv.w + 1.0f);
+        const int j0 = (int)fminf(fmaxf(fj, -2.0f), (float)tv.h + 1.0f);
         const float4 t00 = texel(tv, i0, j0), t10 = texel(tv, i0 + 1, j0);
         const float4 t01 = texel(tv, i0, j0 + 1), t11 = texel(tv, i0 + 1, j0 + 1);
         const float s = 1.0f / 255.0f;
@@ -120,12 +124,12 @@ __device__ __forceinline__ void tri_colour(const TriRecord &r, const long long E
         rgb[1] = ((1.f - ay) * ((1.f - ax) * t00.y + ax * t10.y) + ay * ((1.f - ax) * t01.y + ax * t11.y)) * s;
         rgb[2] = ((1.f - ay) * ((1.f - ax) * t00.z + ax * t10.z) + ay * ((1.f - ax) * t01.z + ax * t11.z)) * s;
     } else if (kind == 0) {
-        const double c0 = l0 * r.q3.x + l1 * r.q3.w + l2 * r.q4.z;
-        const double c1 = l0 * r.q3.y + l1 * r.q4.x + l2 * r.q4.w;
-        const double c2 = l0 * r.q3.z + l1 * r.q4.y + l2 * r.q5.x;
-        rgb[0] = (float)fmin(fmax(c0, 0.0), 1.0);
-        rgb[1] = (float)fmin(fmax(c1, 0.0), 1.0);
-        rgb[2] = (float)fmin(fmax(c2, 0.0), 1.0);
+        const float c0 = l0 * r.q3.x + l1 * r.q3.w + l2 * r.q4.z;
+        const float c1 = l0 * r.q3.y + l1 * r.q4.x + l2 * r.q4.w;
+        const float c2 = l0 * r.q3.z + l1 * r.q4.y + l2 * r.q5.x;
+        rgb[0] = fminf(fmaxf(c0, 0.0f), 1.0f);
+        rgb[1] = fminf(fmaxf(c1, 0.0f), 1.0f);
+        rgb[2] = fminf(fmaxf(c2, 0.0f), 1.0f);
     } else {
         rgb[0] = rgb[1] = rgb[2] = 1.f;
     }
