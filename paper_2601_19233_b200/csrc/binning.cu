@@ -435,17 +435,11 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
 
 // ----------------------------------------------------------------------------
 // One stable onesweep LSD pass on `bits` bits at `shift` (Adinets & Merrill).
-// Tiles of 256 x ITEMS keys, warp-striped; warp-level multisplit ranking with
-// __match_any_sync; keys are moved into shared memory at their block-sorted
+// Tiles of 256 x ITEMS keys, warp-striped; warp-level multisplit ranking from
+// one ballot per digit bit; keys are moved into shared memory at their block-sorted
 // position BEFORE the per-digit decoupled look-back (so no key register is live
 // across it); then a coalesced-by-digit scatter to global memory.
 // ----------------------------------------------------------------------------
-#ifndef UNIMGS_RANK_MATCH
-#define UNIMGS_RANK_MATCH 0
-#endif
-#ifndef UNIMGS_RANK_ATOMS
-#define UNIMGS_RANK_ATOMS 0
-#endif
 #ifndef UNIMGS_SORT_MINB
 #define UNIMGS_SORT_MINB 2
 #endif
@@ -511,10 +505,8 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
             // stable warp multisplit: the lanes holding the same digit
             const bool valid = wbase + 32u * i < n;
             const unsigned d = valid ? (unsigned)((key[i] >> shift) & mask) : 0u;
-#if UNIMGS_RANK_MATCH
-            const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 256u) & __ballot_sync(0xffffffffu, valid);
-#else
-            // all `bits` ballots first (independent), then combine
+            // all `bits` ballots first (independent), then combine (MATCH.ANY costs ~250
+            // SMSP-cycles per warp op on B200, DESIGN.md §5 history)
             unsigned bb[8];
 #pragma unroll
             for (int bt = 0; bt < 8; bt++)
@@ -523,20 +515,10 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
 #pragma unroll
             for (int bt = 0; bt < 8; bt++)
                 if (bt < bits) peers &= ((d >> bt) & 1u) ? bb[bt] : ~bb[bt];
-#endif
-#if UNIMGS_RANK_ATOMS
-            // the group's leader reserves its slots with one shared atomic; in-order per warp,
-            // so earlier items of the same digit are counted first (stable)
-            const int leader = __ffs(peers) - 1;
-            unsigned before = 0;
-            if (valid && lane == (unsigned)leader) before = atomicAdd(&wh[d], (unsigned)__popc(peers));
-            before = __shfl_sync(0xffffffffu, before, valid ? leader : (int)lane);
-#else
             const unsigned before = valid ? wh[d] : 0u;
             __syncwarp();
             if (valid && (peers & lt) == 0) wh[d] = before + __popc(peers);
             __syncwarp();
-#endif
             rank[i] = before + __popc(peers & lt);
         }
         __syncthreads();
