@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gather", action="store_true")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "p2p"],
+                    help="frame gather to rank 0 (N > 1): NCCL send/recv on a comm stream, or the fused "
+                         "variant -- each rank's blend stores its frames into rank 0's buffer over P2P")
     ap.add_argument("--streams", type=int, default=4,
                     help="renderer contexts on separate CUDA streams; consecutive views overlap")
     return ap.parse_args()
@@ -172,7 +175,7 @@ def run_ours(a, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2601_19233_b200 import renderer as R, scenes
-    from paper_2601_19233_b200.dist import gather_frames, views_for_rank
+    from paper_2601_19233_b200.dist import P2PFrameGather, gather_frames, views_for_rank
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -195,13 +198,14 @@ def run_ours(a, rank, world, local_rank):
     recv = None
     if gather and rank == 0:
         recv = [torch.empty((world - 1, V, H, W, 4), dtype=torch.float32, device=dev) for _ in range(2)]
-    comm = torch.cuda.Stream(device=dev) if gather else None
+    p2p = P2PFrameGather(V, H, W, rank, world) if gather and a.gather == "p2p" else None
+    comm = torch.cuda.Stream(device=dev) if gather and p2p is None else None
     s = torch.cuda.current_stream()
 
     def step_fn(step, ev_pairs=None):
         # view j of the step renders with context j % nS on stream j % nS: the
         # compute-bound blend of one view overlaps the binning of the next
-        buf = frames[step & 1]
+        buf = p2p.frames(step) if p2p is not None else frames[step & 1]
         for st_ in streams:
             st_.wait_stream(s)
         for j, vi in enumerate(views_of(step)):
@@ -219,6 +223,9 @@ def run_ours(a, rank, world, local_rank):
         for st_ in streams:
             s.wait_stream(st_)
         if not gather:
+            return []
+        if p2p is not None:  # frames already stored in rank 0's buffer: complete the step
+            p2p.step_done()
             return []
         done = torch.cuda.Event()
         done.record(s)
@@ -333,6 +340,9 @@ def run_ours(a, rank, world, local_rank):
                        "(double-buffered, overlapping the previous step's rendering), views on %d render lanes, "
                        "frames -> pinned host; wall clock from the first call to host_wait" % nS}
 
+    if p2p is not None:
+        p2p.close()
+
     # ---- CPU baseline (oracle), rank 0 at N = 1 only ---------------------------
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -383,7 +393,9 @@ def run_ours(a, rank, world, local_rank):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "views_per_step_per_gpu": V, "image": [W, H],
                    "gaussians": sc.gaussians.count, "triangles": sc.mesh.num_triangles,
-                   "sort_mode": a.sort_mode, "gather": "NCCL send/recv to rank 0" if gather else "none",
+                   "sort_mode": a.sort_mode,
+                   "gather": ("none" if not gather else "NCCL send/recv to rank 0" if p2p is None else
+                              "fused: blend stores into rank 0's buffer over P2P (CUDA IPC)"),
                    "l2": "inputs larger than L2 (scene %.2f GB > 126 MB; per-view K ~7.5M pairs)" % (ds.nbytes() / 1e9),
                    "parallelism": f"views i mod {world}", "streams_per_gpu": nS},
         "frame_ms": frame_ms,

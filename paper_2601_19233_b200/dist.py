@@ -49,3 +49,71 @@ def gathered_view_order(step: int, views_per_step: int, world: int, n_views: int
         if p != dst:
             order.append(views_for_rank(step, views_per_step, p, world, n_views))
     return order
+
+
+class _DevicePtr:
+    """Wraps a raw device pointer as a float32 array (``__cuda_array_interface__``) so
+    torch can view it without a copy."""
+
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 2, "strides": None}
+
+
+class P2PFrameGather:
+    """The fused frame gather (SURVEY §8(e) variant): every rank's blend stores its frames
+    straight into rank 0's frame buffer over NVLink P2P, so no separate collective runs.
+
+    Rank 0 ``cudaMalloc``s buf [2][world][V][H][W][4] (double-buffered by step) and
+    shares one CUDA IPC handle; rank r maps it and passes ``frames(step)`` -- its
+    slot buf[step % 2][r] -- as the ``out`` of ``Renderer.render``, so the blend's
+    epilogue writes the remote frame directly.  ``step_done()`` (device sync +
+    barrier) makes a step's frames complete on rank 0.  No kernel waits on another
+    rank: ranks only store, then meet at a host barrier.
+    """
+
+    def __init__(self, V: int, H: int, W: int, rank: int, world: int, group=None):
+        from cuda.bindings import runtime as rt
+        self.rt, self.rank, self.world, self.group = rt, rank, world, group
+        self.shape = (2, world, V, H, W, 4)
+        nbytes = 4 * 2 * world * V * H * W * 4
+        obj = [None]
+        if rank == 0:
+            err, ptr = rt.cudaMalloc(nbytes)
+            _check(err, "cudaMalloc")
+            err, h = rt.cudaIpcGetMemHandle(ptr)
+            _check(err, "cudaIpcGetMemHandle")
+            self.ptr = int(ptr)
+            obj = [bytes(h.reserved)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        if rank != 0:
+            h = rt.cudaIpcMemHandle_t()
+            h.reserved = obj[0]
+            err, ptr = rt.cudaIpcOpenMemHandle(h, rt.cudaIpcMemLazyEnablePeerAccess)
+            _check(err, "cudaIpcOpenMemHandle")
+            self.ptr = int(ptr)
+        self.buf = torch.as_tensor(_DevicePtr(self.ptr, self.shape), device="cuda")
+
+    def frames(self, step: int) -> torch.Tensor:
+        """This rank's slot of the step: [V, H, W, 4] on rank 0's device memory."""
+        return self.buf[step % 2][self.rank]
+
+    def step_done(self):
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+
+    def close(self):
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        self.buf = None
+        if self.rank != 0:  # importers unmap first; the exporter frees after them
+            self.rt.cudaIpcCloseMemHandle(self.ptr)
+        dist.barrier(group=self.group)
+        if self.rank == 0:
+            self.rt.cudaFree(self.ptr)
+
+
+def _check(err, what):
+    from cuda.bindings import runtime as rt
+    if err != rt.cudaError_t.cudaSuccess:
+        raise RuntimeError(f"{what}: {err}")
