@@ -206,6 +206,13 @@ __device__ __forceinline__ void tri_pixel(Px<MODE, M> &s, const TriRecord &r, in
     const int X[3] = {q0.x, q0.z, q1.x}, Y[3] = {q0.y, q0.w, q1.y};
     long long Ec[3];
     if (COUNT) w_tt++;
+    {   // exact pre-test: no sample (centre +- 16 R in 1/256 px) can lie in the triangle's bbox
+        constexpr int R16 = 16 * (M == 1 ? 0 : M == 2 ? 4 : M == 4 ? 6 : M == 8 ? 7 : 8);
+        const int PX = 256 * x + 128, PY = 256 * y + 128;
+        if (PX + R16 < min(X[0], min(X[1], X[2])) || PX - R16 > max(X[0], max(X[1], X[2])) ||
+            PY + R16 < min(Y[0], min(Y[1], Y[2])) || PY - R16 > max(Y[0], max(Y[1], Y[2])))
+            return;
+    }
     const unsigned m = coverage<M>(X, Y, x, y, Ec);
     if (!m) return;
     if (COUNT) w_tf++;
