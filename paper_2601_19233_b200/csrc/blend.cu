@@ -94,7 +94,8 @@ __device__ __forceinline__ unsigned coverage(const int X[3], const int Y[3], int
 // unclamped barycentrics from the exact centre edge functions, in fp32 (colour
 // only has to meet the 1e-3 tolerance; w_k = E_k z_i z_j has ~6e-8 relative
 // error, far below it), bilinear texture in fp32.
-__device__ __forceinline__ void tri_colour(const TriRecord &r, const long long Ec[3], const TexView &tv, float rgb[3]) {
+__device__ __forceinline__ void tri_colour(const TriRecord &r, int kind, const long long Ec[3], const TexView &tv,
+                                           float rgb[3]) {
     const float z0 = r.q2.x, z1 = r.q2.y, z2 = r.q2.z;
     // w_k = b_k / z_k  ~  E_k * (product of the other two z)
     const float w0 = (float)Ec[0] * (z1 * z2), w1 = (float)Ec[1] * (z0 * z2), w2 = (float)Ec[2] * (z0 * z1);
@@ -107,7 +108,6 @@ __device__ __forceinline__ void tri_colour(const TriRecord &r, const long long E
         const float iA = 1.0f / (float)(Ec[0] + Ec[1] + Ec[2]);
         l0 = (float)Ec[0] * iA; l1 = (float)Ec[1] * iA; l2 = (float)Ec[2] * iA;
     }
-    const int kind = r.q1.z;
     if (kind == 1) {
         const float uu = l0 * r.q3.x + l1 * r.q3.w + l2 * r.q4.z;
         const float vv = l0 * r.q3.y + l1 * r.q4.x + l2 * r.q4.w;
@@ -199,11 +199,12 @@ __device__ __forceinline__ float popc_frac(unsigned m) {
 
 // One triangle fragment candidate at pixel (x, y): coverage, then the mode's update
 // (exact: Eq.7-9 in a depth-adjacent entity).
+// X, Y, kind and alpha come from the warp's staged entry; the rest of the record
+// (depths, attributes) is read only for a covered pixel.
 template <bool COUNT, int MODE, int M>
-__device__ __forceinline__ void tri_pixel(Px<MODE, M> &s, const TriRecord &r, int x, int y, const TexView &tv,
-                                          float t_eps, unsigned long long &w_tt, unsigned long long &w_tf) {
-    const int4 q0 = r.q0, q1 = r.q1;
-    const int X[3] = {q0.x, q0.z, q1.x}, Y[3] = {q0.y, q0.w, q1.y};
+__device__ __forceinline__ void tri_pixel(Px<MODE, M> &s, const int X[3], const int Y[3], int kind, float al,
+                                          const TriRecord &r, int x, int y, const TexView &tv, float t_eps,
+                                          unsigned long long &w_tt, unsigned long long &w_tf) {
     long long Ec[3];
     if (COUNT) w_tt++;
     {   // exact pre-test: no sample (centre +- 16 R in 1/256 px) can lie in the triangle's bbox
@@ -217,8 +218,7 @@ __device__ __forceinline__ void tri_pixel(Px<MODE, M> &s, const TriRecord &r, in
     if (!m) return;
     if (COUNT) w_tf++;
     float rgb[3];
-    tri_colour(r, Ec, tv, rgb);
-    const float al = __int_as_float(q1.w);
+    tri_colour(r, kind, Ec, tv, rgb);
     if (MODE == MODE_NAIVE || MODE == MODE_MSAA_PIXEL) {
         const float O = MODE == MODE_NAIVE ? 1.f : popc_frac<M>(m);  // full / geometric coverage (Eq.5-6)
         const float w = s.T * O * al;
@@ -343,8 +343,11 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
                 buf[slot][1] = make_float4(b.x, b.y + b.y, b.z, __uint_as_float(id));
                 buf[slot][2] = c;
             } else {
-                buf[slot][0] = make_float4(0.f, 0.f, -1.f, 0.f);
-                buf[slot][1] = make_float4(0.f, 0.f, 0.f, __uint_as_float(id));
+                // triangle: q_max = -1 (no Gaussian test passes), the prefetched vertices,
+                // kind and alpha staged with it: (X0, Y0, -1, Y1), (X2, Y2, X1, id), (kind, alpha)
+                buf[slot][0] = make_float4(a.x, a.y, -1.f, a.w);
+                buf[slot][1] = make_float4(b.x, b.y, a.z, __uint_as_float(id));
+                buf[slot][2] = make_float4(b.z, b.w, 0.f, 0.f);
             }
         }
         __syncwarp();
@@ -406,10 +409,15 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
                 const float4 eb = buf[k][1];
                 if (gauss(ea, eb, k)) continue;
                 if (ea.z < 0.f) {
+                    const float4 ec = buf[k][2];
+                    const int X[3] = {__float_as_int(ea.x), __float_as_int(eb.z), __float_as_int(eb.x)};
+                    const int Y[3] = {__float_as_int(ea.y), __float_as_int(ea.w), __float_as_int(eb.y)};
                     const TriRecord &r = trec[__float_as_uint(eb.w)];
 #pragma unroll
                     for (int p = 0; p < PIX; p++)
-                        if (!s[p].done) tri_pixel<COUNT, MODE, M>(s[p], r, x, y0 + 4 * p, tv, bp.t_eps, w_tt, w_tf);
+                        if (!s[p].done)
+                            tri_pixel<COUNT, MODE, M>(s[p], X, Y, __float_as_int(ec.x), ec.y, r, x, y0 + 4 * p, tv,
+                                                      bp.t_eps, w_tt, w_tf);
                 }
             }
         }
