@@ -94,7 +94,12 @@ __device__ __forceinline__ unsigned coverage(const int X[3], const int Y[3], int
 // unclamped barycentrics from the exact centre edge functions, in fp32 (colour
 // only has to meet the 1e-3 tolerance; w_k = E_k z_i z_j has ~6e-8 relative
 // error, far below it), bilinear texture in fp32.
-__device__ __forceinline__ void tri_colour(const TriRecord &r, int kind, const long long Ec[3], const TexView &tv,
+// The record's depth/attribute words q2..q5, staged in shared memory by cp.async.
+struct TriAttr {
+    float4 q2, q3, q4, q5;
+};
+
+__device__ __forceinline__ void tri_colour(const TriAttr &r, int kind, const long long Ec[3], const TexView &tv,
                                            float rgb[3]) {
     const float z0 = r.q2.x, z1 = r.q2.y, z2 = r.q2.z;
     // w_k = b_k / z_k  ~  E_k * (product of the other two z)
@@ -200,10 +205,10 @@ __device__ __forceinline__ float popc_frac(unsigned m) {
 // One triangle fragment candidate at pixel (x, y): coverage, then the mode's update
 // (exact: Eq.7-9 in a depth-adjacent entity).
 // X, Y, kind and alpha come from the warp's staged entry; the rest of the record
-// (depths, attributes) is read only for a covered pixel.
+// (depths, attributes) arrives in shared memory by cp.async at packing time.
 template <bool COUNT, int MODE, int M>
 __device__ __forceinline__ void tri_pixel(Px<MODE, M> &s, const int X[3], const int Y[3], int kind, float al,
-                                          const TriRecord &r, int x, int y, const TexView &tv, float t_eps,
+                                          const TriAttr &r, int x, int y, const TexView &tv, float t_eps,
                                           unsigned long long &w_tt, unsigned long long &w_tf) {
     long long Ec[3];
     if (COUNT) w_tt++;
@@ -275,6 +280,7 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
     constexpr int NW = kBlendThreads / PIX / 32;  // warps per tile
     unsigned long long w_gt = 0, w_gf = 0, w_tt = 0, w_tf = 0;  // COUNT only
     __shared__ float4 s_buf[NW][32][3];  // per-warp packed entries: a (u, v, q_max, o), (ca, 2cb, cc, id), c
+    __shared__ TriAttr s_tri[NW][32];    // a packed triangle entry's q2..q5 (cp.async)
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = (int)__ldg(order + blockIdx.x);  // longest-first schedule (k_tile_order)
@@ -287,6 +293,7 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
     const uint2 rg = ranges[tile];
     const unsigned lt = (1u << lane) - 1u;
     float4(*buf)[3] = s_buf[warp];
+    TriAttr *tat = s_tri[warp];
 
     Px<MODE, M> s[PIX];
 #pragma unroll
@@ -348,6 +355,13 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
                 buf[slot][0] = make_float4(a.x, a.y, -1.f, a.w);
                 buf[slot][1] = make_float4(b.x, b.y, a.z, __uint_as_float(id));
                 buf[slot][2] = make_float4(b.z, b.w, 0.f, 0.f);
+                const char *src = reinterpret_cast<const char *>(&trec[id].q2);
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(&tat[slot]);
+#pragma unroll
+                for (int w = 0; w < 4; w++)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * w), "l"(src + 16 * w)
+                                 : "memory");
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
             }
         }
         __syncwarp();
@@ -404,15 +418,22 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
             }
             if (k < cnt) gauss(buf[k][0], buf[k][1], k);
         } else {
+            bool staged = false;
             for (unsigned k = 0; k < cnt; k++) {
                 const float4 ea = buf[k][0];
                 const float4 eb = buf[k][1];
-                if (gauss(ea, eb, k)) continue;
-                if (ea.z < 0.f) {
+                if (ea.z >= 0.f) {  // warp-uniform: entry k is the same for every lane
+                    gauss(ea, eb, k);
+                } else {
+                    if (!staged) {  // the chunk's triangle attributes, waited for once
+                        asm volatile("cp.async.wait_all;\n" ::: "memory");
+                        __syncwarp();
+                        staged = true;
+                    }
                     const float4 ec = buf[k][2];
                     const int X[3] = {__float_as_int(ea.x), __float_as_int(eb.z), __float_as_int(eb.x)};
                     const int Y[3] = {__float_as_int(ea.y), __float_as_int(ea.w), __float_as_int(eb.y)};
-                    const TriRecord &r = trec[__float_as_uint(eb.w)];
+                    const TriAttr &r = tat[k];
 #pragma unroll
                     for (int p = 0; p < PIX; p++)
                         if (!s[p].done)
