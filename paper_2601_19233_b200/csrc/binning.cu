@@ -443,12 +443,13 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
 #ifndef UNIMGS_SORT_MINB
 #define UNIMGS_SORT_MINB 2
 #endif
-template <typename KT, int ITEMS>
+template <typename KT, int ITEMS, int NB>
 __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MINB)) k_onesweep(const KT *__restrict__ kin,
                                                               const uint32_t *__restrict__ vin, KT *__restrict__ kout,
                                                               uint32_t *__restrict__ vout, const unsigned *n_ptr,
-                                                              int shift, int bits, const unsigned *hist, int slot,
+                                                              int shift, const unsigned *hist, int slot,
                                                               unsigned long long *lb, DevState *st) {
+    static_assert(NB >= 1 && NB <= 8, "digit width");
     constexpr int TILE_ = kSortThreads * ITEMS;
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned *s_wh = reinterpret_cast<unsigned *>(smem);           // [8][256]
@@ -456,12 +457,15 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
     int *s_glob = reinterpret_cast<int *>(s_doff + 256);            // [256] global base - local offset
     unsigned *s_hex = reinterpret_cast<unsigned *>(s_glob + 256);   // [256] global exclusive histogram
     unsigned *s_misc = s_hex + 256;                                 // [16]
-    KT *s_k = reinterpret_cast<KT *>(s_misc + 16);
-    uint32_t *s_v = reinterpret_cast<uint32_t *>(s_k + TILE_);
+    // two stages of (keys[TILE_], vals[TILE_]): the next tile's input arrives by
+    // cp.async while this one is ranked; a stage, once in registers, is reused as
+    // the block-sorted staging of its own tile's scatter
+    unsigned char *s_stage = reinterpret_cast<unsigned char *>(s_misc + 16);
+    constexpr unsigned kStageBytes = TILE_ * (sizeof(KT) + sizeof(uint32_t));
 
     const unsigned n = *n_ptr;
     const unsigned tag = epoch_tag(st, slot);
-    const unsigned mask = (1u << bits) - 1u;
+    constexpr unsigned mask = (1u << NB) - 1u;
     const unsigned t = threadIdx.x, lane = t & 31, wid = t >> 5;
 
     // global exclusive digit offsets (block scan of the histogram, 1 digit per thread)
@@ -480,12 +484,40 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
         s_hex[t] = x - h + add;
     }
 
-    while (true) {
-        const unsigned tile = claim_tile(&st->ctr[slot], &s_misc[1]);
-        if ((unsigned long long)tile * TILE_ >= n) break;
+    // cp.async one tile's keys and values (16-byte chunks, zero-filled past n;
+    // tile bases are 16-byte aligned: TILE_ items into 256-byte aligned buffers)
+    auto issue = [&](unsigned tl, int sb) {
+        unsigned char *dst = s_stage + sb * kStageBytes;
+        const unsigned long long b0 = (unsigned long long)tl * TILE_;
+        const unsigned long long nv = n - b0 < (unsigned long long)TILE_ ? n - b0 : (unsigned long long)TILE_;
+        const char *ks = reinterpret_cast<const char *>(kin + b0);
+        const char *vs = reinterpret_cast<const char *>(vin + b0);
+        constexpr unsigned KC = TILE_ * sizeof(KT) / 16, VC = TILE_ * sizeof(uint32_t) / 16;
+        const long long kb = (long long)(nv * sizeof(KT)), vb = (long long)(nv * sizeof(uint32_t));
+        for (unsigned c = t; c < KC + VC; c += kSortThreads) {
+            const bool isk = c < KC;
+            const unsigned cc = isk ? c : c - KC;
+            const long long rem = (isk ? kb : vb) - 16ll * cc;
+            const unsigned sz = rem <= 0 ? 0u : rem >= 16 ? 16u : (unsigned)rem;
+            const char *src = (isk ? ks : vs) + (sz ? 16ull * cc : 0ull);
+            const unsigned d = (unsigned)__cvta_generic_to_shared(dst + (isk ? 0u : TILE_ * sizeof(KT)) + 16u * cc);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(sz) : "memory");
+        }
+    };
+    unsigned tile = claim_tile(&st->ctr[slot], &s_misc[1]);
+    int sb = 0;
+    if ((unsigned long long)tile * TILE_ < n) issue(tile, 0);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    while ((unsigned long long)tile * TILE_ < n) {
+        const unsigned next = claim_tile(&st->ctr[slot], &s_misc[1]);
+        if ((unsigned long long)next * TILE_ < n) issue(next, sb ^ 1);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
         const unsigned base = tile * (unsigned)TILE_;
         for (int i = t; i < 8 * 256; i += kSortThreads) s_wh[i] = 0;
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // this tile's stage
         __syncthreads();
+        KT *s_k = reinterpret_cast<KT *>(s_stage + sb * kStageBytes);
+        uint32_t *s_v = reinterpret_cast<uint32_t *>(s_k + TILE_);
 
         KT key[ITEMS];
         uint32_t val[ITEMS];
@@ -495,26 +527,26 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
         unsigned *wh = s_wh + wid * 256;
 #pragma unroll
         for (int i = 0; i < ITEMS; i++) {
-            const unsigned idx = wbase + 32u * i;
-            const bool valid = idx < n;
-            key[i] = valid ? kin[idx] : (KT)0;
-            val[i] = valid ? vin[idx] : 0u;
+            const unsigned li = wid * 32u * ITEMS + lane + 32u * i;
+            key[i] = s_k[li];  // zero-filled past n
+            val[i] = s_v[li];
         }
 #pragma unroll
         for (int i = 0; i < ITEMS; i++) {
             // stable warp multisplit: the lanes holding the same digit
             const bool valid = wbase + 32u * i < n;
             const unsigned d = valid ? (unsigned)((key[i] >> shift) & mask) : 0u;
-            // all `bits` ballots first (independent), then combine (MATCH.ANY costs ~250
+            // one ballot per digit bit, NB fixed at compile time (MATCH.ANY costs ~250
             // SMSP-cycles per warp op on B200, DESIGN.md §5 history)
-            unsigned bb[8];
-#pragma unroll
-            for (int bt = 0; bt < 8; bt++)
-                if (bt < bits) bb[bt] = __ballot_sync(0xffffffffu, (d >> bt) & 1u);
             unsigned peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
-            for (int bt = 0; bt < 8; bt++)
-                if (bt < bits) peers &= ((d >> bt) & 1u) ? bb[bt] : ~bb[bt];
+            for (int bt = 0; bt < NB; bt++)  // peers &= bit ? ballot : ~ballot, 4 instructions per bit
+                asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+                    "and.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
+                    "vote.sync.ballot.b32 t, p, 0xffffffff;\n\t"
+                    "@!p not.b32 t, t;\n\tand.b32 %0, %0, t;\n\t}"
+                    : "+r"(peers)
+                    : "r"(d), "r"(1u << bt));
             const unsigned before = valid ? wh[d] : 0u;
             __syncwarp();
             if (valid && (peers & lt) == 0) wh[d] = before + __popc(peers);
@@ -591,6 +623,8 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
             kout[o] = kk;
             vout[o] = s_v[k];
         }
+        tile = next;
+        sb ^= 1;
     }
 }
 
@@ -642,7 +676,7 @@ __global__ void k_ranges64(const unsigned long long *__restrict__ keys, const un
 
 template <typename KT, int ITEMS>
 static size_t onesweep_smem() {
-    return (8 * 256 + 256 * 3 + 16) * sizeof(unsigned) + kSortThreads * ITEMS * (sizeof(KT) + sizeof(uint32_t));
+    return (8 * 256 + 256 * 3 + 16) * sizeof(unsigned) + 2 * kSortThreads * ITEMS * (sizeof(KT) + sizeof(uint32_t));
 }
 #ifndef UNIMGS_DEPTH_ITEMS
 #define UNIMGS_DEPTH_ITEMS 8
@@ -656,29 +690,40 @@ static int bits_for(int64_t tiles) {
     return b;
 }
 
+template <typename KT, int ITEMS, int NB>
+static void onesweep_launch(Buffers &b, const KT *kin, const uint32_t *vin, KT *kout, uint32_t *vout,
+                            const unsigned *n_ptr, int shift, int hist_row, int slot, int grid, cudaStream_t s) {
+    static const bool attr = [] {  // dynamic shared memory above 48 KB, once per instantiation (thread-safe)
+        cudaFuncSetAttribute(k_onesweep<KT, ITEMS, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)onesweep_smem<KT, ITEMS>());
+        return true;
+    }();
+    (void)attr;
+    k_onesweep<KT, ITEMS, NB><<<grid, kSortThreads, onesweep_smem<KT, ITEMS>(), s>>>(
+        kin, vin, kout, vout, n_ptr, shift, &b.st->hist[hist_row][0], slot, b.lookback, b.st);
+}
+
 template <typename KT, int ITEMS = kSortItems>
 static void onesweep_pass(Buffers &b, const KT *kin, const uint32_t *vin, KT *kout, uint32_t *vout,
                           const unsigned *n_ptr, int shift, int bits, int hist_row, int slot, int grid,
                           cudaStream_t s) {
-    k_onesweep<KT, ITEMS><<<grid, kSortThreads, onesweep_smem<KT, ITEMS>(), s>>>(
-        kin, vin, kout, vout, n_ptr, shift, bits, &b.st->hist[hist_row][0], slot, b.lookback, b.st);
+#define UNIMGS_OS(NB) onesweep_launch<KT, ITEMS, NB>(b, kin, vin, kout, vout, n_ptr, shift, hist_row, slot, grid, s)
+    switch (bits) {
+        case 1: UNIMGS_OS(1); break;
+        case 2: UNIMGS_OS(2); break;
+        case 3: UNIMGS_OS(3); break;
+        case 4: UNIMGS_OS(4); break;
+        case 5: UNIMGS_OS(5); break;
+        case 6: UNIMGS_OS(6); break;
+        case 7: UNIMGS_OS(7); break;
+        default: UNIMGS_OS(8); break;
+    }
+#undef UNIMGS_OS
 }
 
 static int sort_grid(int64_t max_items, int sm_count, int per_sm, int tile = kSortTile) {
     const int64_t tiles = (max_items + tile - 1) / tile;
     return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count * per_sm));
-}
-
-static void set_attrs() {
-    static bool done = false;
-    if (done) return;
-    cudaFuncSetAttribute(k_onesweep<uint16_t, kSortItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)onesweep_smem<uint16_t, kSortItems>());
-    cudaFuncSetAttribute(k_onesweep<uint32_t, kDepthItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)onesweep_smem<uint32_t, kDepthItems>());
-    cudaFuncSetAttribute(k_onesweep<unsigned long long, kSortItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)onesweep_smem<unsigned long long, kSortItems>());
-    done = true;
 }
 
 // Blend schedule (longest first): the hardware hands out CTAs in blockIdx order,
@@ -721,7 +766,6 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2 *__restrict__ r
 int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam, int sort_mode, int tri_depth,
                cudaStream_t s, int sm_count) {
     (void)N;
-    set_attrs();
     int launches = 0;
     const int64_t tiles = (int64_t)cam.tiles_x * cam.tiles_y;
     const int tb = bits_for(tiles);
