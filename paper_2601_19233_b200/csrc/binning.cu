@@ -457,11 +457,8 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
     int *s_glob = reinterpret_cast<int *>(s_doff + 256);            // [256] global base - local offset
     unsigned *s_hex = reinterpret_cast<unsigned *>(s_glob + 256);   // [256] global exclusive histogram
     unsigned *s_misc = s_hex + 256;                                 // [16]
-    // two stages of (keys[TILE_], vals[TILE_]): the next tile's input arrives by
-    // cp.async while this one is ranked; a stage, once in registers, is reused as
-    // the block-sorted staging of its own tile's scatter
-    unsigned char *s_stage = reinterpret_cast<unsigned char *>(s_misc + 16);
-    constexpr unsigned kStageBytes = TILE_ * (sizeof(KT) + sizeof(uint32_t));
+    KT *s_k = reinterpret_cast<KT *>(s_misc + 16);
+    uint32_t *s_v = reinterpret_cast<uint32_t *>(s_k + TILE_);
 
     const unsigned n = *n_ptr;
     const unsigned tag = epoch_tag(st, slot);
@@ -484,40 +481,12 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
         s_hex[t] = x - h + add;
     }
 
-    // cp.async one tile's keys and values (16-byte chunks, zero-filled past n;
-    // tile bases are 16-byte aligned: TILE_ items into 256-byte aligned buffers)
-    auto issue = [&](unsigned tl, int sb) {
-        unsigned char *dst = s_stage + sb * kStageBytes;
-        const unsigned long long b0 = (unsigned long long)tl * TILE_;
-        const unsigned long long nv = n - b0 < (unsigned long long)TILE_ ? n - b0 : (unsigned long long)TILE_;
-        const char *ks = reinterpret_cast<const char *>(kin + b0);
-        const char *vs = reinterpret_cast<const char *>(vin + b0);
-        constexpr unsigned KC = TILE_ * sizeof(KT) / 16, VC = TILE_ * sizeof(uint32_t) / 16;
-        const long long kb = (long long)(nv * sizeof(KT)), vb = (long long)(nv * sizeof(uint32_t));
-        for (unsigned c = t; c < KC + VC; c += kSortThreads) {
-            const bool isk = c < KC;
-            const unsigned cc = isk ? c : c - KC;
-            const long long rem = (isk ? kb : vb) - 16ll * cc;
-            const unsigned sz = rem <= 0 ? 0u : rem >= 16 ? 16u : (unsigned)rem;
-            const char *src = (isk ? ks : vs) + (sz ? 16ull * cc : 0ull);
-            const unsigned d = (unsigned)__cvta_generic_to_shared(dst + (isk ? 0u : TILE_ * sizeof(KT)) + 16u * cc);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(sz) : "memory");
-        }
-    };
-    unsigned tile = claim_tile(&st->ctr[slot], &s_misc[1]);
-    int sb = 0;
-    if ((unsigned long long)tile * TILE_ < n) issue(tile, 0);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-    while ((unsigned long long)tile * TILE_ < n) {
-        const unsigned next = claim_tile(&st->ctr[slot], &s_misc[1]);
-        if ((unsigned long long)next * TILE_ < n) issue(next, sb ^ 1);
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    while (true) {
+        const unsigned tile = claim_tile(&st->ctr[slot], &s_misc[1]);
+        if ((unsigned long long)tile * TILE_ >= n) break;
         const unsigned base = tile * (unsigned)TILE_;
         for (int i = t; i < 8 * 256; i += kSortThreads) s_wh[i] = 0;
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // this tile's stage
         __syncthreads();
-        KT *s_k = reinterpret_cast<KT *>(s_stage + sb * kStageBytes);
-        uint32_t *s_v = reinterpret_cast<uint32_t *>(s_k + TILE_);
 
         KT key[ITEMS];
         uint32_t val[ITEMS];
@@ -527,9 +496,10 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
         unsigned *wh = s_wh + wid * 256;
 #pragma unroll
         for (int i = 0; i < ITEMS; i++) {
-            const unsigned li = wid * 32u * ITEMS + lane + 32u * i;
-            key[i] = s_k[li];  // zero-filled past n
-            val[i] = s_v[li];
+            const unsigned idx = wbase + 32u * i;
+            const bool valid = idx < n;
+            key[i] = valid ? kin[idx] : (KT)0;
+            val[i] = valid ? vin[idx] : 0u;
         }
 #pragma unroll
         for (int i = 0; i < ITEMS; i++) {
@@ -623,8 +593,6 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
             kout[o] = kk;
             vout[o] = s_v[k];
         }
-        tile = next;
-        sb ^= 1;
     }
 }
 
@@ -676,7 +644,7 @@ __global__ void k_ranges64(const unsigned long long *__restrict__ keys, const un
 
 template <typename KT, int ITEMS>
 static size_t onesweep_smem() {
-    return (8 * 256 + 256 * 3 + 16) * sizeof(unsigned) + 2 * kSortThreads * ITEMS * (sizeof(KT) + sizeof(uint32_t));
+    return (8 * 256 + 256 * 3 + 16) * sizeof(unsigned) + kSortThreads * ITEMS * (sizeof(KT) + sizeof(uint32_t));
 }
 #ifndef UNIMGS_DEPTH_ITEMS
 #define UNIMGS_DEPTH_ITEMS 8
