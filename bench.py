@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--gather", default="nccl", choices=["nccl", "p2p"],
                     help="frame gather to rank 0 (N > 1): NCCL send/recv on a comm stream, or the fused "
                          "variant -- each rank's blend stores its frames into rank 0's buffer over P2P")
+    ap.add_argument("--prio", type=int, default=1, help="1: preprocess+bin on high-priority streams (0: one stream per context)")
     ap.add_argument("--streams", type=int, default=4,
                     help="renderer contexts on separate CUDA streams; consecutive views overlap")
     return ap.parse_args()
@@ -187,6 +188,11 @@ def run_ours(a, rank, world, local_rank):
                      sort_mode=a.sort_mode) for _ in range(nS)]
     r = rs[0]
     streams = [torch.cuda.Stream(device=dev) for _ in range(nS)]
+    # --prio: each context's preprocess + bin on a high-priority stream, its blend on
+    # the normal one, so the latency-bound sort passes of one view get SMs ahead of
+    # the queued CTAs of another view's compute-bound blend
+    # (torch maps a priority beyond the device's range to its highest priority)
+    pstreams = [torch.cuda.Stream(device=dev, priority=-100) for _ in range(nS)] if a.prio else streams
     ds = R.to_device(sc, dev)
     V = a.views
 
@@ -209,9 +215,13 @@ def run_ours(a, rank, world, local_rank):
         for st_ in streams:
             st_.wait_stream(s)
         for j, vi in enumerate(views_of(step)):
-            rr, ss_ = rs[j % nS], streams[j % nS]
-            rr.preprocess(ds, sc.cameras[vi], stream=ss_)
-            rr.bin(stream=ss_)
+            rr, ss_, ps_ = rs[j % nS], streams[j % nS], pstreams[j % nS]
+            if ps_ is not ss_:
+                ps_.wait_stream(ss_)  # the context's previous blend has released its buffers
+            rr.preprocess(ds, sc.cameras[vi], stream=ps_)
+            rr.bin(stream=ps_)
+            if ps_ is not ss_:
+                ss_.wait_stream(ps_)
             if ev_pairs is not None:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(ss_)
@@ -370,7 +380,11 @@ def run_ours(a, rank, world, local_rank):
     props = _t.cuda.get_device_properties(dev)
     sm_count = props.multi_processor_count
     peak_tops = sm_count * 128 * 1.965e9 / 1e12  # 4 schedulers x 32 lanes x max clock
-    achieved = ops / (blend_max / 1000.0) / 1e12
+    # achieved: the blend timed alone (CUDA events on its stream, single-stream pass right
+    # after the timed region).  Inside the timed region each blend launch shares the GPU
+    # with the other contexts' blends and the high-priority sort passes, so its event
+    # bracket measures co-scheduling, not the kernel; that figure is kept as in_region_*.
+    achieved = ops / (blend_iso_ms / 1000.0) / 1e12
     traffic, ncu_issue = None, None
     tp = os.path.join(ROOT, "profiles", "blend_traffic.json")
     if os.path.exists(tp):
@@ -397,19 +411,22 @@ def run_ours(a, rank, world, local_rank):
                    "gather": ("none" if not gather else "NCCL send/recv to rank 0" if p2p is None else
                               "fused: blend stores into rank 0's buffer over P2P (CUDA IPC)"),
                    "l2": "inputs larger than L2 (scene %.2f GB > 126 MB; per-view K ~7.5M pairs)" % (ds.nbytes() / 1e9),
-                   "parallelism": f"views i mod {world}", "streams_per_gpu": nS},
+                   "parallelism": f"views i mod {world}", "streams_per_gpu": nS,
+                   "prio_streams": bool(a.prio)},
         "frame_ms": frame_ms,
         "roofline": {"bound": "alu", "kernel": "k_blend", "achieved": achieved, "peak": peak_tops,
                      "unit": "Tops/s", "frac": achieved / peak_tops, "traffic": traffic,
-                     "ops_per_launch": ops, "avg_launch_ms": blend_max,
-                     "isolated_avg_launch_ms": blend_iso_ms,
-                     "isolated_frac": ops / (blend_iso_ms / 1000.0) / 1e12 / peak_tops,
+                     "ops_per_launch": ops, "avg_launch_ms": blend_iso_ms,
+                     "in_region_avg_launch_ms": blend_max,
+                     "in_region_frac": ops / (blend_max / 1000.0) / 1e12 / peak_tops,
                      "fragment_ops_per_launch": frag_ops,
-                     "fragments_only_isolated_frac": frag_ops / (blend_iso_ms / 1000.0) / 1e12 / peak_tops,
+                     "fragments_only_frac": frag_ops / (blend_iso_ms / 1000.0) / 1e12 / peak_tops,
                      "work_note": "ops = pixel-entry tests x test ops + fragments x blend ops (DESIGN.md §5)",
                      "ncu_issue": ncu_issue,
-                     "timing_note": f"avg_launch_ms from CUDA events on the launching streams inside the timed "
-                                    f"region ({nS} overlapped streams); isolated_* from a single-stream pass",
+                     "timing_note": f"avg_launch_ms: CUDA events on the launching stream, the blend alone "
+                                    f"(single-stream pass over the timed views, right after the timed region); "
+                                    f"in_region_*: the same events inside the timed region, where each launch "
+                                    f"shares the GPU with {nS - 1} other contexts and the high-priority sorts",
                      "peak_note": f"{sm_count} SMs x 4 schedulers x 32 lanes x 1965 MHz (issue-slot lane-ops)",
                      "work_per_launch": {k: v / n_blend for k, v in work.items()}},
         "hbm": {"alg_bytes_per_frame": bytes_alg / len(timed_views), "achieved_gbs": hbm_gbs,

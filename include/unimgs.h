@@ -289,7 +289,10 @@ UNIMGS_API int unimgs_render_host(unimgs_ctx *c, const unimgs_gaussians *g_host,
  * without synchronising.  The context keeps two device copies of the scene,
  * so the host->device upload of this call (on an internal copy stream) runs
  * while the previous call still renders on `stream`, and the frame read-backs
- * run on a third stream.  The host input arrays and out_host must stay valid
+ * run on a third stream.  Each view's preprocess + bin run on an internal
+ * highest-priority stream of its lane (joined to `stream` by events), so the
+ * latency-bound sort of one lane is scheduled ahead of the queued blend CTAs
+ * of another.  The host input arrays and out_host must stay valid
  * and unmodified until unimgs_host_wait returns (or, for the inputs, until
  * the call after next has been issued).  Capacity overflow is reported by
  * unimgs_host_wait.  unimgs_render_host == render_host_async + host_wait. */

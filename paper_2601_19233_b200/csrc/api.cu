@@ -47,6 +47,11 @@ struct unimgs_ctx {
     unimgs_ctx *child[kMaxLanes] = {};
     cudaStream_t lane_stream[kMaxLanes] = {};
     cudaEvent_t ev_lane_done[kMaxLanes] = {};
+    // per lane context: preprocess + bin on a high-priority stream, so the
+    // latency-bound sort passes of one lane get SMs ahead of the queued CTAs of
+    // another lane's compute-bound blend (DESIGN.md §5 history)
+    cudaStream_t bin_stream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_binned = nullptr;
 };
 
 extern "C" void unimgs_destroy(unimgs_ctx *c);
@@ -488,6 +493,13 @@ extern "C" int unimgs_render_host_async(unimgs_ctx *c, const unimgs_gaussians *g
                 CUDA_TRY(c, cudaEventCreateWithFlags(&x->ev_render[i], cudaEventDisableTiming));
                 CUDA_TRY(c, cudaEventCreateWithFlags(&x->ev_copy[i], cudaEventDisableTiming));
             }
+        if (!x->bin_stream) {
+            int lo = 0, hi = 0;
+            CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CUDA_TRY(c, cudaStreamCreateWithPriority(&x->bin_stream, cudaStreamNonBlocking, hi));
+            CUDA_TRY(c, cudaEventCreateWithFlags(&x->ev_ready, cudaEventDisableTiming));
+            CUDA_TRY(c, cudaEventCreateWithFlags(&x->ev_binned, cudaEventDisableTiming));
+        }
     }
     char *p = (char *)c->stage_buf[slot];
     char *dp[11];
@@ -518,10 +530,20 @@ extern "C" int unimgs_render_host_async(unimgs_ctx *c, const unimgs_gaussians *g
         unimgs_ctx *x = l ? c->child[l] : c;  // lane 0 is this context on the caller's stream
         cudaStream_t ls = l ? c->lane_stream[l] : s;
         const int bi = (v / c->lanes) & 1;
+        // preprocess + bin on the lane's high-priority stream after everything before
+        // on the lane (the upload, the lane's previous blend), the blend back on ls
+        CUDA_TRY(c, cudaEventRecord(x->ev_ready, ls));
+        CUDA_TRY(c, cudaStreamWaitEvent(x->bin_stream, x->ev_ready, 0));
+        int rc = unimgs_preprocess(x, &gd, &md, &cams[v], x->bin_stream);
+        if (!rc) rc = unimgs_bin(x, x->bin_stream);
+        if (rc) {
+            if (x != c) c->err = x->err;
+            return rc;
+        }
+        CUDA_TRY(c, cudaEventRecord(x->ev_binned, x->bin_stream));
+        CUDA_TRY(c, cudaStreamWaitEvent(ls, x->ev_binned, 0));
         CUDA_TRY(c, cudaStreamWaitEvent(ls, x->ev_copy[bi], 0));  // frame buffer drained (no-op if never recorded)
-        int rc = unimgs_preprocess(x, &gd, &md, &cams[v], ls);
-        if (!rc) rc = unimgs_bin(x, ls);
-        if (!rc) rc = unimgs_render(x, x->frames[bi], ls);
+        rc = unimgs_render(x, x->frames[bi], ls);
         if (rc) {
             if (x != c) c->err = x->err;
             return rc;
@@ -626,5 +648,11 @@ extern "C" void unimgs_destroy(unimgs_ctx *c) {
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->up_stream) cudaStreamDestroy(c->up_stream);
+    if (c->bin_stream) {
+        cudaStreamSynchronize(c->bin_stream);
+        cudaStreamDestroy(c->bin_stream);
+        cudaEventDestroy(c->ev_ready);
+        cudaEventDestroy(c->ev_binned);
+    }
     delete c;
 }
