@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--gather", default="nccl", choices=["nccl", "p2p"],
                     help="frame gather to rank 0 (N > 1): NCCL send/recv on a comm stream, or the fused "
                          "variant -- each rank's blend stores its frames into rank 0's buffer over P2P")
+    ap.add_argument("--sort-ctas-per-sm", type=int, default=-1, help="-1: 1 with several streams, else auto")
     ap.add_argument("--prio", type=int, default=1, help="1: preprocess+bin on high-priority streams (0: one stream per context)")
     ap.add_argument("--streams", type=int, default=4,
                     help="renderer contexts on separate CUDA streams; consecutive views overlap")
@@ -184,8 +185,11 @@ def run_ours(a, rank, world, local_rank):
     n_orbit = len(sc.cameras)
     W, H = sc.cameras[0].width, sc.cameras[0].height
     nS = max(1, a.streams)
+    # several contexts render concurrently: one sort CTA per SM leaves the rest of
+    # each SM to the other contexts' blends (settings.sort_ctas_per_sm)
+    spm = a.sort_ctas_per_sm if a.sort_ctas_per_sm >= 0 else (1 if nS > 1 else 0)
     rs = [R.Renderer(sc.gaussians.count, sc.mesh.num_triangles, 20 << 20, W, H, bg=tuple(float(v) for v in sc.bg),
-                     sort_mode=a.sort_mode) for _ in range(nS)]
+                     sort_mode=a.sort_mode, sort_ctas_per_sm=spm) for _ in range(nS)]
     r = rs[0]
     streams = [torch.cuda.Stream(device=dev) for _ in range(nS)]
     # --prio: each context's preprocess + bin on a high-priority stream, its blend on
@@ -412,7 +416,7 @@ def run_ours(a, rank, world, local_rank):
                               "fused: blend stores into rank 0's buffer over P2P (CUDA IPC)"),
                    "l2": "inputs larger than L2 (scene %.2f GB > 126 MB; per-view K ~7.5M pairs)" % (ds.nbytes() / 1e9),
                    "parallelism": f"views i mod {world}", "streams_per_gpu": nS,
-                   "prio_streams": bool(a.prio)},
+                   "prio_streams": bool(a.prio), "sort_ctas_per_sm": spm},
         "frame_ms": frame_ms,
         "roofline": {"bound": "alu", "kernel": "k_blend", "achieved": achieved, "peak": peak_tops,
                      "unit": "Tops/s", "frac": achieved / peak_tops, "traffic": traffic,

@@ -152,7 +152,13 @@ typedef struct {
  *   1 = per (tile, triangle) pair: the view z of its plane at the tile centre,
  *       clamped to the triangle's z range (N8) -- interpenetrating
  *       surfaces swap order across tiles.  Per-pair keys need the full 64-bit
- *       sort, so tri_depth 1 always bins as sort_mode 1.                     */
+ *       sort, so tri_depth 1 always bins as sort_mode 1.
+ * sort_ctas_per_sm: persistent CTAs per SM of the radix-sort passes, 1..4, or
+ *   0 = automatic (4 for a context rendering alone; 1 for the contexts of a
+ *   unimgs_render_host call with several lanes).  4 gives the lowest latency
+ *   for one frame; 1 leaves 3/4 of every SM to the blends of other contexts
+ *   rendering concurrently, the higher multi-view throughput.
+ *   Scheduling only: the output is identical for every value.              */
 typedef struct {
     int32_t msaa_samples, tile_size;
     float alpha_min, alpha_max, t_eps, dilation;
@@ -160,6 +166,7 @@ typedef struct {
     int32_t sort_mode;
     int32_t blend_mode;
     int32_t tri_depth;
+    int32_t sort_ctas_per_sm;
 } unimgs_settings;
 
 typedef struct {

@@ -55,7 +55,7 @@ class Settings(C.Structure):
     _fields_ = [("msaa_samples", C.c_int32), ("tile_size", C.c_int32), ("alpha_min", C.c_float),
                 ("alpha_max", C.c_float), ("t_eps", C.c_float), ("dilation", C.c_float), ("bg", C.c_float * 3),
                 ("bg_alpha", C.c_float), ("sort_mode", C.c_int32), ("blend_mode", C.c_int32),
-                ("tri_depth", C.c_int32)]
+                ("tri_depth", C.c_int32), ("sort_ctas_per_sm", C.c_int32)]
 
 
 class Stats(C.Structure):

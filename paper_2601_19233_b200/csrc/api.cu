@@ -26,6 +26,7 @@ struct unimgs_ctx {
     CamParams cam{};
     int64_t P = 0;
     int sort_mode_used = 0;
+    int sort_per_sm_auto = 4;  // sort_ctas_per_sm = 0: 4 alone, 1 with several host lanes
     int sm_count = 148;
     int64_t launches = 0;
     std::string err;
@@ -94,6 +95,7 @@ extern "C" void unimgs_default_settings(unimgs_settings *s) {
     s->sort_mode = 0;
     s->blend_mode = 0;
     s->tri_depth = 0;
+    s->sort_ctas_per_sm = 0;
 }
 
 static int validate_settings(unimgs_ctx *c, const unimgs_settings *s) {
@@ -110,6 +112,8 @@ static int validate_settings(unimgs_ctx *c, const unimgs_settings *s) {
     if (!(s->dilation >= 0.f && std::isfinite(s->dilation))) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "dilation < 0");
     if (s->sort_mode != 0 && s->sort_mode != 1) return fail(c, UNIMGS_ERR_UNSUPPORTED, "sort_mode must be 0 or 1");
     if (s->tri_depth != 0 && s->tri_depth != 1) return fail(c, UNIMGS_ERR_UNSUPPORTED, "tri_depth must be 0 or 1");
+    if (s->sort_ctas_per_sm < 0 || s->sort_ctas_per_sm > 4)
+        return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "sort_ctas_per_sm must be 0..4");
     for (int i = 0; i < 3; i++)
         if (!std::isfinite(s->bg[i])) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "bg not finite");
     if (!std::isfinite(s->bg_alpha)) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "bg_alpha not finite");
@@ -172,7 +176,7 @@ extern "C" int unimgs_reserve2(unimgs_ctx *c, int64_t max_gaussians, int64_t max
     Buffers &b = c->buf;
     const int64_t P = max_gaussians + max_triangles + 1;
     const int64_t tiles = (int64_t)((max_w + 15) / 16) * ((max_h + 15) / 16);
-    const int64_t lb_tiles = std::max<int64_t>((max_pairs + 4095) / 4096, (P + 2047) / 2048) + 2;
+    const int64_t lb_tiles = sort_lookback_tiles(max_pairs, P);
     CUDA_TRY(c, cudaMalloc(&b.rect, sizeof(uint2) * P));
     CUDA_TRY(c, cudaMalloc(&b.touched, sizeof(uint32_t) * P));
     CUDA_TRY(c, cudaMalloc(&b.dkey, sizeof(uint32_t) * P));
@@ -295,7 +299,8 @@ extern "C" int unimgs_bin(unimgs_ctx *c, void *stream) {
     if (c->stage < 1) return fail(c, UNIMGS_ERR_STATE, "bin before preprocess");
     c->sort_mode_used = c->set.tri_depth ? 1 : c->set.sort_mode;  // per-pair triangle keys need the full sort
     c->launches += launch_bin(c->buf, c->P, c->g.N, c->m.F, c->cam, c->sort_mode_used, c->set.tri_depth,
-                              (cudaStream_t)stream, c->sm_count);
+                              (cudaStream_t)stream, c->sm_count,
+                              c->set.sort_ctas_per_sm ? c->set.sort_ctas_per_sm : c->sort_per_sm_auto);
     int rc = check_launch(c, "bin");
     if (rc) return rc;
     c->stage = 2;
@@ -594,6 +599,7 @@ extern "C" int unimgs_set_host_lanes(unimgs_ctx *c, int32_t lanes) {
         c->child[l] = nullptr;
     }
     c->lanes = 1;
+    c->sort_per_sm_auto = lanes > 1 ? 1 : 4;
     for (int l = 1; l < lanes; l++) {
         int rc = unimgs_create(&c->child[l], &c->set);
         if (!rc) rc = unimgs_reserve2(c->child[l], c->max_g, c->max_t, c->max_pairs, c->max_w, c->max_h);
@@ -602,6 +608,7 @@ extern "C" int unimgs_set_host_lanes(unimgs_ctx *c, int32_t lanes) {
             c->child[l] = nullptr;
             return fail(c, rc, "set_host_lanes: lane %d allocation failed", l);
         }
+        c->child[l]->sort_per_sm_auto = 1;
         CUDA_TRY(c, cudaStreamCreateWithFlags(&c->lane_stream[l], cudaStreamNonBlocking));
         CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_lane_done[l], cudaEventDisableTiming));
         c->lanes = l + 1;

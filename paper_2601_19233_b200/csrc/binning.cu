@@ -37,11 +37,11 @@
 
 #include "internal.cuh"
 
-#ifndef UNIMGS_SORT_PER_SM
-#define UNIMGS_SORT_PER_SM 2  // persistent sort-pass CTAs per SM
+#ifndef UNIMGS_EXPAND_PER_SM
+#define UNIMGS_EXPAND_PER_SM 4  // k_expand CTAs per SM (persistent over slot ranges)
 #endif
 #ifndef UNIMGS_SORT_ITEMS
-#define UNIMGS_SORT_ITEMS 16
+#define UNIMGS_SORT_ITEMS 8
 #endif
 
 namespace unimgs {
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
 // across it); then a coalesced-by-digit scatter to global memory.
 // ----------------------------------------------------------------------------
 #ifndef UNIMGS_SORT_MINB
-#define UNIMGS_SORT_MINB 2
+#define UNIMGS_SORT_MINB 4  // 64 registers: a sort CTA holds a quarter of the SM's register file
 #endif
 template <typename KT, int ITEMS, int NB>
 __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MINB)) k_onesweep(const KT *__restrict__ kin,
@@ -652,6 +652,12 @@ static size_t onesweep_smem() {
 constexpr int kDepthItems = UNIMGS_DEPTH_ITEMS;  // small depth sort: short tiles, latency-bound
 
 
+int64_t sort_lookback_tiles(int64_t max_pairs, int64_t max_prims) {
+    const int64_t pair_tiles = (max_pairs + kSortTile - 1) / kSortTile;
+    const int64_t prim_tiles = (max_prims + kSortThreads * kDepthItems - 1) / (kSortThreads * kDepthItems);
+    return std::max<int64_t>(pair_tiles, prim_tiles) + 2;
+}
+
 static int bits_for(int64_t tiles) {
     int b = 0;
     while (((int64_t)1 << b) < tiles) b++;
@@ -732,7 +738,7 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2 *__restrict__ r
 }
 
 int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam, int sort_mode, int tri_depth,
-               cudaStream_t s, int sm_count) {
+               cudaStream_t s, int sm_count, int sort_per_sm) {
     (void)N;
     int launches = 0;
     const int64_t tiles = (int64_t)cam.tiles_x * cam.tiles_y;
@@ -754,7 +760,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         // depth sort of the visible primitives
         k_hist_depth<<<sm_count * 2, 256, 0, s>>>(b.pk[0], b.st);
         launches++;
-        const int g1 = sort_grid(P, sm_count, kDepthItems <= 4 ? 4 : UNIMGS_SORT_PER_SM, kSortThreads * kDepthItems);
+        const int g1 = sort_grid(P, sm_count, sort_per_sm, kSortThreads * kDepthItems);
         int cur = 0;
         for (int pass = 0; pass < 4; pass++, slot++) {
             onesweep_pass<uint32_t, kDepthItems>(b, b.pk[cur], b.pv[cur], b.pk[cur ^ 1], b.pv[cur ^ 1], &b.st->n_vis,
@@ -777,8 +783,8 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
                          s>>>(b.dcnt, prel, slots, b.rstart, b.st);
         launches++;
     }
-    const int egrid = (int)std::max<int64_t>(1, std::min<int64_t>((b.max_pairs + 1023) / 1024, sm_count * 4));
-    const int g2 = sort_grid(b.max_pairs, sm_count, UNIMGS_SORT_PER_SM);
+    const int egrid = (int)std::max<int64_t>(1, std::min<int64_t>((b.max_pairs + 1023) / 1024, sm_count * UNIMGS_EXPAND_PER_SM));
+    const int g2 = sort_grid(b.max_pairs, sm_count, sort_per_sm);
     if (!full) {
         k_expand<false><<<egrid, kScanThreads, 0, s>>>(dup_ids, b.rect, b.dkey, b.dcnt, prel, b.rstart, cam.tiles_x,
                                                         b.trec, (unsigned)F, 0, b.tk[0], b.tv[0], b.st);

@@ -130,8 +130,12 @@ int launch_preprocess_gaussians(const GaussInput &g, int64_t F, const CamParams 
                                 const Buffers &b, cudaStream_t s);
 int launch_setup_triangles(const MeshInput &m, const CamParams &cam, const Buffers &b, cudaStream_t s);
 // binning: factored (sort_mode 0) or full 64-bit keys (sort_mode 1)
+// Look-back rows the sort passes need (one per sort tile of the largest pass).
+int64_t sort_lookback_tiles(int64_t max_pairs, int64_t max_prims);
+// sort_per_sm: persistent CTAs per SM of the sort passes (1..4; registers are capped
+// at 64 so four fit beside nothing else, one leaves 3/4 of the SM to other streams)
 int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam, int sort_mode, int tri_depth,
-               cudaStream_t s, int sm_count);
+               cudaStream_t s, int sm_count, int sort_per_sm);
 int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, const CamParams &cam,
                  const BlendParams &bp, float *out, cudaStream_t s, bool count_work = false);
 int launch_tile_stats(const Buffers &b, int tiles, cudaStream_t s);

@@ -111,11 +111,12 @@ EXACT, NAIVE, MSAA_PIXEL, WHOLE_PIXEL, PAPER_LITERAL = range(5)  # blend modes (
 
 
 def make_settings(alpha_max=0.99, t_eps=1e-4, dilation=0.3, bg=(0.0, 0.0, 0.0), bg_alpha=1.0,
-                  sort_mode=0, blend_mode=EXACT, msaa=4, tri_depth=0) -> _lib.Settings:
+                  sort_mode=0, blend_mode=EXACT, msaa=4, tri_depth=0, sort_ctas_per_sm=0) -> _lib.Settings:
     s = _lib.Settings()
     _lib.load().unimgs_default_settings(C.byref(s))
     s.alpha_max, s.t_eps, s.dilation, s.bg_alpha, s.sort_mode = alpha_max, t_eps, dilation, bg_alpha, sort_mode
     s.blend_mode, s.msaa_samples, s.tri_depth = blend_mode, msaa, tri_depth
+    s.sort_ctas_per_sm = sort_ctas_per_sm
     for i in range(3):
         s.bg[i] = float(bg[i])
     return s

@@ -291,9 +291,31 @@ def test_junk_is_invisible_on_gpu(built):
     assert st["culled_guard_band"] > stb["culled_guard_band"]
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+def test_sort_ctas_per_sm_agree(built, mode):
+    """settings.sort_ctas_per_sm only schedules: 1..4 persistent sort CTAs per SM
+    give bit-identical bins and images (K ~1.8M: several sort tiles per persistent CTA)."""
+    import torch
+    from paper_2601_19233_b200 import renderer as R
+    sc = scenes.make_random(7, n_gauss=60000, n_tris=2000, W=640, H=360)
+    ds = R.to_device(sc)
+    outs = []
+    for spm in (0, 1, 2, 3, 4):
+        r = R.renderer_for(sc, max_pairs=4 << 20, sort_mode=mode, sort_ctas_per_sm=spm)
+        img = r.render_view(ds, sc.cameras[0]).clone()
+        outs.append((img, r.bins()))
+    torch.cuda.synchronize()
+    assert outs[0][1][0].size > 148 * 2048  # several sort tiles per persistent CTA
+    for img, bins in outs[1:]:
+        assert torch.equal(outs[0][0], img)
+        for a, b in zip(outs[0][1], bins):
+            assert np.array_equal(a, b)
+
+
 def test_multiview_bench_launch_configuration(built, oracle_mod):
     """The bench's launch configuration at full size: 3M-Gaussian multiview scene,
-    views round-robin on 3 contexts / streams concurrently (bench.py step_fn).
+    views round-robin on 3 contexts concurrently (bench.py step_fn): one sort CTA
+    per SM, preprocess + bin on high-priority streams, blends on normal ones.
     Every frame equals the single-context render of its view bit for bit, and one
     of them matches the oracle on sampled tiles."""
     import torch
@@ -305,14 +327,21 @@ def test_multiview_bench_launch_configuration(built, oracle_mod):
     views = [3, 40, 77, 114, 151, 188]
     nS = 3
     rs = [R.Renderer(sc.gaussians.count, sc.mesh.num_triangles, 20 << 20, W, H,
-                     bg=tuple(float(v) for v in sc.bg), bg_alpha=float(sc.bg_alpha)) for _ in range(nS)]
+                     bg=tuple(float(v) for v in sc.bg), bg_alpha=float(sc.bg_alpha), sort_ctas_per_sm=1)
+          for _ in range(nS)]
     streams = [torch.cuda.Stream() for _ in range(nS)]
+    pstreams = [torch.cuda.Stream(priority=-100) for _ in range(nS)]
     out = torch.empty((len(views), H, W, 4), device="cuda")
     s = torch.cuda.current_stream()
     for st_ in streams:
         st_.wait_stream(s)
     for j, vi in enumerate(views):
-        rs[j % nS].render_view(ds, sc.cameras[vi], out=out[j], stream=streams[j % nS])
+        rr, ss_, ps_ = rs[j % nS], streams[j % nS], pstreams[j % nS]
+        ps_.wait_stream(ss_)
+        rr.preprocess(ds, sc.cameras[vi], stream=ps_)
+        rr.bin(stream=ps_)
+        ss_.wait_stream(ps_)
+        rr.render(out[j], stream=ss_)
     for st_ in streams:
         s.wait_stream(st_)
     torch.cuda.synchronize()
