@@ -112,7 +112,10 @@ __device__ __forceinline__ void sh_eval(const float *__restrict__ sh, int deg, f
 }
 
 // B1: one thread per Gaussian (N1-N5).
-__global__ void __launch_bounds__(256) k_preprocess_gaussians(GaussInput gin, int64_t F, CamParams cam, float dilation,
+#ifndef UNIMGS_PRE_MINB
+#define UNIMGS_PRE_MINB 5  // 48 registers: 5 CTAs per SM
+#endif
+__global__ void __launch_bounds__(256, UNIMGS_PRE_MINB) k_preprocess_gaussians(GaussInput gin, int64_t F, CamParams cam, float dilation,
                                                              Buffers b) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool vis = false;
