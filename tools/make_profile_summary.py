@@ -55,7 +55,10 @@ def main():
     lines += ["## Launch list: kernel shares of a frame (ncu gpu__time_duration, cold-cache, serialised)", "",
               f"Command: `ncu --metrics gpu__time_duration.sum --clock-control none --csv {cmd}`; "
               f"{frames} frames (k_begin_frame launches) over the warm-up, timed, isolated-blend and "
-              "work-counting passes; `k_blend<1,...>` is the counting variant of the last pass.", "",
+              "work-counting passes; `k_blend<1,...>` is the counting variant of the last pass.  The bench's "
+              "4 concurrent contexts run the sort passes at 1 CTA/SM (`settings.sort_ctas_per_sm`, which leaves "
+              "the rest of each SM to the other contexts' blends), so serialised under ncu they show their "
+              "stand-alone latency; the full capture below is one frame of a single context (4 CTAs/SM).", "",
               "| kernel | launches | mean us | us per frame | share of frame |", "|---|---|---|---|---|"]
     for k, v in per.items():
         lines.append(f"| {k} | {len(v)} | {sum(v) / len(v) / 1e3:.1f} | {frame_us[k] / 1e3:.1f} | "
