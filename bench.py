@@ -234,18 +234,34 @@ def run_ours(a, rank, world, local_rank):
                 ev_pairs.append((e0, e1))
             else:
                 rr.render(buf[j], stream=ss_)
-        for st_ in streams:
-            s.wait_stream(st_)
+        # No join at the end of a step: the next step's views queue behind this one's on
+        # each context's streams (steps pipeline like the iterations of a serving loop);
+        # the timed region joins all streams once, before its end event.
         if not gather:
             return []
         if p2p is not None:  # frames already stored in rank 0's buffer: complete the step
+            for st_ in streams:
+                s.wait_stream(st_)
             p2p.step_done()
             return []
-        done = torch.cuda.Event()
-        done.record(s)
+        # the gather of step k waits for its own views only; the caller's wait() on the
+        # handles (on s, which every stream waits on at the next step's start) keeps
+        # step k + 2 from overwriting this step's frame buffer before it has left
+        evs = []
+        for st_ in streams:
+            e = torch.cuda.Event()
+            e.record(st_)
+            evs.append(e)
         with torch.cuda.stream(comm):
-            comm.wait_event(done)
+            for e in evs:
+                comm.wait_event(e)
             return gather_frames(buf, recv[step & 1] if rank == 0 else None, rank, world)
+
+    def join():
+        for st_ in streams:
+            s.wait_stream(st_)
+        if comm is not None:
+            s.wait_stream(comm)
 
     # warm-up (also validates capacity)
     pending = []
@@ -255,6 +271,7 @@ def run_ours(a, rank, world, local_rank):
         pending = step_fn(w)
     for q in pending:
         q.wait()
+    join()
     torch.cuda.synchronize()
     st = r.stats()
     assert st["overflow"] == 0 and all(x.stats()["overflow"] == 0 for x in rs)
@@ -298,6 +315,7 @@ def run_ours(a, rank, world, local_rank):
         pending = new
     for q in pending:
         q.wait()
+    join()
     t_end.record(s)
     torch.cuda.synchronize()
     if world > 1:

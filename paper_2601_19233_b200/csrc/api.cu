@@ -47,7 +47,7 @@ struct unimgs_ctx {
     int lanes = 1;
     unimgs_ctx *child[kMaxLanes] = {};
     cudaStream_t lane_stream[kMaxLanes] = {};
-    cudaEvent_t ev_lane_done[kMaxLanes] = {};
+    cudaEvent_t ev_lane_free[2][kMaxLanes] = {};  // lane l done with scene slot i
     // per lane context: preprocess + bin on a high-priority stream, so the
     // latency-bound sort passes of one lane get SMs ahead of the queued CTAs of
     // another lane's compute-bound blend (DESIGN.md §5 history)
@@ -518,7 +518,10 @@ extern "C" int unimgs_render_host_async(unimgs_ctx *c, const unimgs_gaussians *g
                             (size_t)F * 12, (size_t)F * 4,
                             tex ? (size_t)mh->tex_width * mh->tex_height * 4 : 0};
     // upload on its own stream, once the call two back (same buffer) has rendered
-    if (c->host_calls >= 2) CUDA_TRY(c, cudaStreamWaitEvent(c->up_stream, c->ev_stage_free[slot], 0));
+    if (c->host_calls >= 2) {
+        CUDA_TRY(c, cudaStreamWaitEvent(c->up_stream, c->ev_stage_free[slot], 0));
+        for (int l = 1; l < c->lanes; l++) CUDA_TRY(c, cudaStreamWaitEvent(c->up_stream, c->ev_lane_free[slot][l], 0));
+    }
     for (int i = 0; i < 11; i++)
         if (src[i] && bytes[i])
             CUDA_TRY(c, cudaMemcpyAsync(dp[i], src[i], bytes[i], cudaMemcpyHostToDevice, c->up_stream));
@@ -560,8 +563,8 @@ extern "C" int unimgs_render_host_async(unimgs_ctx *c, const unimgs_gaussians *g
         CUDA_TRY(c, cudaEventRecord(x->ev_copy[bi], c->copy_stream));
     }
     for (int l = 1; l < c->lanes; l++) {  // the scene slot is free once every lane has rendered
-        CUDA_TRY(c, cudaEventRecord(c->ev_lane_done[l], c->lane_stream[l]));
-        CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_lane_done[l], 0));
+        // (no join onto `stream`: only the upload two calls later waits for these)
+        CUDA_TRY(c, cudaEventRecord(c->ev_lane_free[slot][l], c->lane_stream[l]));
     }
     CUDA_TRY(c, cudaEventRecord(c->ev_stage_free[slot], s));
     c->host_calls++;
@@ -595,7 +598,7 @@ extern "C" int unimgs_set_host_lanes(unimgs_ctx *c, int32_t lanes) {
     for (int l = 1; l < c->lanes; l++) {  // drop the previous lanes
         unimgs_destroy(c->child[l]);
         cudaStreamDestroy(c->lane_stream[l]);
-        cudaEventDestroy(c->ev_lane_done[l]);
+        for (int i = 0; i < 2; i++) cudaEventDestroy(c->ev_lane_free[i][l]);
         c->child[l] = nullptr;
     }
     c->lanes = 1;
@@ -610,7 +613,7 @@ extern "C" int unimgs_set_host_lanes(unimgs_ctx *c, int32_t lanes) {
         }
         c->child[l]->sort_per_sm_auto = 1;
         CUDA_TRY(c, cudaStreamCreateWithFlags(&c->lane_stream[l], cudaStreamNonBlocking));
-        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_lane_done[l], cudaEventDisableTiming));
+        for (int i = 0; i < 2; i++) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_lane_free[i][l], cudaEventDisableTiming));
         c->lanes = l + 1;
     }
     return UNIMGS_OK;
@@ -641,7 +644,7 @@ extern "C" void unimgs_destroy(unimgs_ctx *c) {
         cudaStreamSynchronize(c->lane_stream[l]);
         unimgs_destroy(c->child[l]);
         cudaStreamDestroy(c->lane_stream[l]);
-        cudaEventDestroy(c->ev_lane_done[l]);
+        for (int i = 0; i < 2; i++) cudaEventDestroy(c->ev_lane_free[i][l]);
     }
     free_buffers(c);
     if (c->copy_stream) cudaDeviceSynchronize();
