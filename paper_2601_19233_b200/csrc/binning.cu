@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
                                                          const uint32_t *__restrict__ prel,
                                                          const uint32_t *__restrict__ rstart, int tiles_x,
                                                          const TriRecord *__restrict__ trec, unsigned F, int tri_depth,
-                                                         void *tk_, uint32_t *tv, DevState *st) {
+                                                         int lo_bits, void *tk_, uint32_t *tv, DevState *st) {
     using Key = typename DupCfg<FULL>::Key;
     constexpr int SLOTS = ExpandCfg<FULL>::SLOTS, PER = ExpandCfg<FULL>::PER, MP = SLOTS + 2;
     __shared__ int s_off[MP];          // primitive start slot relative to the range (first may be < 0)
@@ -403,8 +403,9 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
                     s_k[k] = (Key)t;
                 }
                 s_v[k] = pid;
-                atomicAdd(&s_hl[t & 255u], 1u);
-                atomicAdd(&s_hh[(t >> 8) & 255u], 1u);
+                // sort_mode 0 splits the tile id into lo_bits + the rest (balanced digits)
+                atomicAdd(&s_hl[FULL ? t & 255u : t & ((1u << lo_bits) - 1u)], 1u);
+                atomicAdd(&s_hh[FULL ? (t >> 8) & 255u : (t >> lo_bits) & 255u], 1u);
                 if (FULL) {
                     if (t >= 65536u) atomicAdd(&s_h3[FULL ? (t >> 16) & 255u : 0], 1u);
                     else n_h3_zero++;  // third tile digit 0, added once per thread below
@@ -786,12 +787,17 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
     const int egrid = (int)std::max<int64_t>(1, std::min<int64_t>((b.max_pairs + 1023) / 1024, sm_count * UNIMGS_EXPAND_PER_SM));
     const int g2 = sort_grid(b.max_pairs, sm_count, sort_per_sm);
     if (!full) {
+        // balanced digits (13 tile bits at 1080p: 7 + 6, not 8 + 5): fewer buckets per
+        // 2048-key sort tile, so longer runs in each pass's scatter
+        const int npass = (tb + 7) / 8, lo_bits = npass > 1 ? (tb + npass - 1) / npass : std::max(tb, 1);
         k_expand<false><<<egrid, kScanThreads, 0, s>>>(dup_ids, b.rect, b.dkey, b.dcnt, prel, b.rstart, cam.tiles_x,
-                                                        b.trec, (unsigned)F, 0, b.tk[0], b.tv[0], b.st);
+                                                        b.trec, (unsigned)F, 0, lo_bits, b.tk[0], b.tv[0], b.st);
         launches++;
-        for (int pass = 0, sh = 0; sh < tb; pass++, sh += 8, slot++) {
+        for (int pass = 0, sh = 0; sh < tb; pass++, slot++) {
+            const int nb = pass == 0 ? lo_bits : tb - sh;
             onesweep_pass<uint16_t>(b, (const uint16_t *)b.tk[tc], b.tv[tc], (uint16_t *)b.tk[tc ^ 1], b.tv[tc ^ 1],
-                                    &b.st->K, sh, std::min(8, tb - sh), HIST_TILE0 + pass, slot, g2, s);
+                                    &b.st->K, sh, nb, HIST_TILE0 + pass, slot, g2, s);
+            sh += nb;
             tc ^= 1;
             launches++;
         }
@@ -800,7 +806,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         launches++;
     } else {
         k_expand<true><<<egrid, kScanThreads, 0, s>>>(dup_ids, b.rect, b.dkey, b.dcnt, prel, b.rstart, cam.tiles_x,
-                                                       b.trec, (unsigned)F, tri_depth, b.tk[0], b.tv[0], b.st);
+                                                       b.trec, (unsigned)F, tri_depth, 8, b.tk[0], b.tv[0], b.st);
         launches++;
         const int total_bits = 32 + tb;
         for (int pass = 0, sh = 0; sh < total_bits; pass++, sh += 8, slot++) {
