@@ -182,7 +182,12 @@ struct Px {
     float t[M];
     float G, Tl;
     float Tx;  // cached exit transmittance of the open entity (refreshed by each triangle)
+    float py;  // pixel centre y for the Gaussian test; NaN once done (the test then fails by itself)
     bool open, done;
+    __device__ __forceinline__ void finish() {
+        done = true;
+        py = __int_as_float(0x7fc00000);
+    }
     __device__ __forceinline__ float mean_t() const {
         float a = 0.f;
 #pragma unroll
@@ -229,7 +234,7 @@ __device__ __forceinline__ void tri_pixel(Px<MODE, M> &s, const int X[3], const 
         const float w = s.T * O * al;
         s.C0 += w * rgb[0]; s.C1 += w * rgb[1]; s.C2 += w * rgb[2];
         s.T -= w;
-        if (s.T < t_eps) s.done = true;
+        if (s.T < t_eps) s.finish();
         return;
     }
     if (!s.open) {
@@ -252,7 +257,7 @@ __device__ __forceinline__ void tri_pixel(Px<MODE, M> &s, const int X[3], const 
         if ((m >> j) & 1u) s.t[j] *= kk;  // Eq.7
     if (MODE == MODE_PAPER_LITERAL) s.Tl *= 1.f - popc_frac<M>(m) * al;
     s.Tx = s.exit_T();
-    if (s.Tx < t_eps) s.done = true;
+    if (s.Tx < t_eps) s.finish();
 }
 
 // One CTA per 16x16 tile, independent warps, PIX pixels per lane (vertically
@@ -303,7 +308,9 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
 #pragma unroll
         for (int j = 0; j < M; j++) s[p].t[j] = 1.f;
         s[p].open = false;
-        s[p].done = !(x < W && y0 + 4 * p < H);
+        s[p].done = false;
+        s[p].py = (float)(y0 + 4 * p) + 0.5f;
+        if (!(x < W && y0 + 4 * p < H)) s[p].finish();
     }
     auto all_done = [&]() {
         bool d = true;
@@ -374,9 +381,9 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
             float q[PIX];
 #pragma unroll
             for (int p = 0; p < PIX; p++) {
-                const float dy = __fsub_rn((float)(y0 + 4 * p) + 0.5f, ea.y);
+                const float dy = __fsub_rn(s[p].py, ea.y);
                 q[p] = __fmaf_rn(eb.x, dxx, __fmaf_rn(eb.z, __fmul_rn(dy, dy), __fmul_rn(eb.y, __fmul_rn(dx, dy))));
-                hit[p] = q[p] <= ea.z && !s[p].done;
+                hit[p] = q[p] <= ea.z;  // false once done: py is NaN
                 if (COUNT && ea.z >= 0.f && !s[p].done) w_gt++;
                 any = any || hit[p];
             }
@@ -394,7 +401,7 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
                     const float w = base * s[p].G * al;
                     s[p].C0 += w * ec.x; s[p].C1 += w * ec.y; s[p].C2 += w * ec.z;
                     s[p].G *= 1.f - al;
-                    if (base * s[p].G < bp.t_eps) s[p].done = true;
+                    if (base * s[p].G < bp.t_eps) s[p].finish();
                     continue;
                 }
                 if (MODE != MODE_NAIVE && MODE != MODE_MSAA_PIXEL && s[p].open) {
@@ -404,7 +411,7 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
                 const float w = s[p].T * al;
                 s[p].C0 += w * ec.x; s[p].C1 += w * ec.y; s[p].C2 += w * ec.z;
                 s[p].T -= w;
-                if (s[p].T < bp.t_eps) s[p].done = true;
+                if (s[p].T < bp.t_eps) s[p].finish();
             }
             return true;
         };
