@@ -68,3 +68,23 @@ def test_no_device_calls_fail_cleanly_without_gpu():
     s.msaa_samples = 3  # only 1, 2, 4, 8, 16
     h = ctypes.c_void_p()
     assert L.unimgs_create(ctypes.byref(h), ctypes.byref(s)) == _lib.ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("field,value,code", [
+    ("msaa_samples", 3, "ERR_UNSUPPORTED"), ("blend_mode", 5, "ERR_UNSUPPORTED"),
+    ("tile_size", 8, "ERR_UNSUPPORTED"), ("sort_mode", 2, "ERR_UNSUPPORTED"),
+    ("tri_depth", 2, "ERR_UNSUPPORTED"), ("sort_ctas_per_sm", 5, "ERR_INVALID_ARGUMENT"),
+    ("sort_ctas_per_sm", -1, "ERR_INVALID_ARGUMENT"), ("alpha_max", 0.0, "ERR_INVALID_ARGUMENT"),
+    ("t_eps", 1.0, "ERR_INVALID_ARGUMENT"), ("dilation", -0.1, "ERR_INVALID_ARGUMENT"),
+])
+def test_create_rejects_invalid_settings(field, value, code):
+    """unimgs_create validates the settings on the host before touching the GPU
+    (include/unimgs.h settings contract): no context, the documented status."""
+    from paper_2601_19233_b200 import _lib
+    L = _lib.load()
+    s = _lib.Settings()
+    L.unimgs_default_settings(ctypes.byref(s))
+    setattr(s, field, value)
+    h = ctypes.c_void_p()
+    assert L.unimgs_create(ctypes.byref(h), ctypes.byref(s)) == getattr(_lib, code)
+    assert not h.value

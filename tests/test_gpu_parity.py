@@ -120,6 +120,10 @@ def test_invalid_arguments(built):
     assert e.value.code == _lib.ERR_INVALID_ARGUMENT
     with pytest.raises(_lib.UnimgsError) as e:
         R.Renderer(10, 10, 100, 64, 64, sort_mode=7)
+    for bad in (-1, 5):  # persistent sort CTAs per SM: 0 (auto) .. 4
+        with pytest.raises(_lib.UnimgsError) as e:
+            R.Renderer(10, 10, 100, 64, 64, sort_ctas_per_sm=bad)
+        assert e.value.code == _lib.ERR_INVALID_ARGUMENT
 
 
 def test_cuda_graph_replay_matches_eager(built):
