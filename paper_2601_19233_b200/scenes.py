@@ -555,6 +555,93 @@ def make_degenerate(seed=13, W=96, H=80):
 
 
 # ----------------------------------------------------------------------------
+# pin constructions for the shading steps (bilinear texture, SH view direction,
+# 1.3x FoV Jacobian clamp).  Geometry and inputs only; the expected values are
+# derived in the tests.
+# ----------------------------------------------------------------------------
+
+AFFINE_TEX = dict(tw=16, th=12, r=(10, 14, 0), g=(7, 0, 20), b=(100, 5, -6))  # value = c0 + ci*i + cj*j
+
+
+def affine_texture(seed=21) -> np.ndarray:
+    """[th, tw, 4] RGBA8 whose RGB is affine in the texel index (i, j): c0 + ci*i + cj*j."""
+    tw, th = AFFINE_TEX["tw"], AFFINE_TEX["th"]
+    j, i = np.meshgrid(np.arange(th), np.arange(tw), indexing="ij")
+    tex = np.empty((th, tw, 4), np.uint8)
+    for ch, key in enumerate("rgb"):
+        c0, ci, cj = AFFINE_TEX[key]
+        tex[..., ch] = c0 + ci * i + cj * j
+    tex[..., 3] = np.random.default_rng(seed).integers(0, 256, (th, tw))  # ignored (R13)
+    return tex
+
+
+def make_texture_quad(x0=5.0, y0=3.0, wq=37.0, hq=29.0, W=48, H=40, texture=None, z=1.0) -> Scene:
+    """Fronto-parallel 2-triangle quad covering pixels [x0, x0+wq] x [y0, y0+hq] with
+    uv (0,0) at (x0, y0) and (1,1) at the far corner (fx = fy = 1 camera at the origin,
+    so one world unit at z = 1 is one pixel and vertices on the 1/256 grid snap exactly).
+    Default: the affine texture stretched by a non-integer factor, so pixel centres land
+    at arbitrary texel fractions."""
+    cam = Camera(W, H, 1.0, 1.0, 0.0, 0.0, np.eye(3, dtype=np.float32), np.zeros(3, np.float32))
+    P = np.array([[x0, y0, 1], [x0 + wq, y0, 1], [x0 + wq, y0 + hq, 1], [x0, y0 + hq, 1]], np.float64) * [z, z, z]
+    uv = np.array([[0, 0], [1, 0], [1, 1], [0, 1]], np.float32)
+    tex = affine_texture() if texture is None else texture
+    mesh = Mesh(P.astype(np.float32), np.array([[0, 1, 2], [0, 2, 3]], np.int32), np.ones(2, np.float32),
+                uvs=uv, texture=tex)
+    return Scene("texquad", empty_gaussians(0), mesh, [cam], bg=np.zeros(3, np.float32))
+
+
+SH_PROBE_K = 0.8  # the degree-1 coefficient: channel r <- basis 1 (y), g <- basis 2 (z), b <- basis 3 (x)
+
+
+def make_sh_probe(seed=22, n=24) -> Scene:
+    """Degree-1 Gaussians whose only non-zero SH coefficients are SH_PROBE_K on the three
+    degree-1 basis functions (one per channel, DC = 0), seen by look-at cameras from
+    above, below, left, right, in front and behind (eyes recorded in the scene name
+    order).  Each camera looks at the cluster centre."""
+    rng = np.random.default_rng(seed)
+    centre = np.array([0.3, -0.2, 0.5])
+    means = centre + rng.uniform(-0.35, 0.35, (n, 3))
+    sh = np.zeros((n, 4, 3), np.float32)
+    sh[:, 1, 0] = sh[:, 2, 1] = sh[:, 3, 2] = SH_PROBE_K
+    g = _pack_gaussians(means, _quats(rng, n), np.full((n, 3), 0.05), np.full(n, 0.9), sh, 1)
+    eyes = [centre + d for d in ([0, 3.0, 0.4], [0, -3.0, 0.4], [-3.0, 0.2, 0.3], [3.0, -0.1, 0.2],
+                                 [0.2, 0.3, -3.0], [-0.3, 0.1, 3.0])]
+    cams = [look_at(e, centre, up=(0, 0, 1) if abs(e[1] - centre[1]) > 1 else (0, 1, 0),
+                    width=96, height=80, fx=80.0, fy=80.0, cx=48.3, cy=39.6) for e in eyes]
+    sc = Scene("sh_probe", g, empty_mesh(), cams, bg=np.zeros(3, np.float32))
+    sc.eyes = [np.asarray(e, np.float64) for e in eyes]
+    return sc
+
+
+FOV_CAM = dict(W=96, H=64, f=64.0)  # 1.3 x half-FoV: |x/z| <= 0.975, |y/z| <= 0.65 (not equal: a W/H swap shows)
+
+
+def make_fov_clamp(seed=23) -> Scene:
+    """Large Gaussians whose centres lie inside and outside the 1.3x tan-FoV cone
+    (R18, the 3DGS Jacobian clamp) yet whose footprints reach the image: camera-space
+    (x/z, y/z) = (0.9, 0) [inside x, outside a height-based limit], (1.1, 0.1), (-1.2, -0.2)
+    [clamped in x], (0.1, 0.75), (-0.3, -0.8) [clamped in y], (1.05, 0.7) [both].  The
+    camera is rotated and translated so W = R_w2c is not the identity."""
+    rng = np.random.default_rng(seed)
+    W, H, f = FOV_CAM["W"], FOV_CAM["H"], FOV_CAM["f"]
+    ang = 0.35
+    ax = np.array([0.2, 1.0, -0.3]) / np.linalg.norm([0.2, 1.0, -0.3])
+    K = np.array([[0, -ax[2], ax[1]], [ax[2], 0, -ax[0]], [-ax[1], ax[0], 0]])
+    Rc = np.eye(3) + np.sin(ang) * K + (1 - np.cos(ang)) * K @ K
+    t = np.array([0.2, -0.1, 0.4])
+    cam = Camera(W, H, f, f, W / 2.0, H / 2.0, Rc.astype(np.float32), t.astype(np.float32))
+    dirs = [(0.9, 0.0), (1.1, 0.1), (-1.2, -0.2), (0.1, 0.75), (-0.3, -0.8), (1.05, 0.7)]
+    z = 3.0
+    pc = np.array([[a * z, b * z, z] for a, b in dirs])
+    Rf, tf = Rc.astype(np.float32).astype(np.float64), t.astype(np.float32).astype(np.float64)
+    means = (pc - tf) @ Rf  # R^T (pc - t), row-wise
+    n = len(dirs)
+    sh = np.zeros((n, 1, 3), np.float32)
+    g = _pack_gaussians(means, _quats(rng, n), rng.uniform(0.3, 0.6, (n, 3)), np.full(n, 0.9), sh, 0)
+    return Scene("fov_clamp", g, empty_mesh(), [cam], bg=np.zeros(3, np.float32))
+
+
+# ----------------------------------------------------------------------------
 # deformation inputs (SURVEY §8(f) row 2; Eq.12-13, P:403-436): a bound proxy mesh
 # and a per-vertex transform field.  Synthetic: random nearby faces with Dirichlet
 # barycentrics stand in for the ray-cast binding; a twist/bend field stands in for
