@@ -208,7 +208,9 @@ UNIMGS_API int unimgs_preprocess(unimgs_ctx *c, const unimgs_gaussians *g, const
                       const unimgs_camera *cam, void *stream);
 
 /* Duplicate (tile, primitive) pairs, sort them by (tile, depth bits, id) and
- * compute per-tile ranges.  Must follow unimgs_preprocess. */
+ * compute per-tile ranges.  Exactly once per unimgs_preprocess (the
+ * per-frame counters it consumes are reset only by preprocess): a second bin
+ * without a new preprocess returns UNIMGS_ERR_STATE and enqueues nothing. */
 UNIMGS_API int unimgs_bin(unimgs_ctx *c, void *stream);
 
 /* B8: the unified single-pass blend (Eq.1-2, 7-11).  Writes
@@ -220,6 +222,8 @@ UNIMGS_API int unimgs_render(unimgs_ctx *c, float *out_rgbt, void *stream);
  * blend (Delta, log R, S) barycentrically at each bound anchor (Eq.12), then
  * R' = exp(mean log R_i), S' = mean S_i, Sigma' = R'S' Sigma (R'S')^T,
  * mu' = mu + mean Delta_i (Eq.13).  Sigma from rest->cov3d or quats/scales.
+ * Device data is culled as values: an anchor whose face is outside [0, F) or
+ * has a vertex id outside [0, V) (V = field->num_vertices) is skipped.
  * Writes means_out [N][3] and cov_out [N][6] (device; pass them as means and
  * cov3d of the next unimgs_preprocess).  No context, no allocation, no sync. */
 UNIMGS_API int unimgs_deform(const unimgs_gaussians *rest, const unimgs_binding *binding,
@@ -306,7 +310,10 @@ UNIMGS_API int unimgs_render_host(unimgs_ctx *c, const unimgs_gaussians *g_host,
 UNIMGS_API int unimgs_render_host_async(unimgs_ctx *c, const unimgs_gaussians *g_host, const unimgs_mesh *m_host,
                                         const unimgs_camera *cams, int32_t n_views, float *out_host, void *stream);
 
-/* Render lanes of the host path (1..8, default 1): lanes - 1 child contexts,
+/* (render_host_async validates every host pointer, count and camera before it
+ * enqueues anything; cov3d, when given, is uploaded in place of quats/scales.)
+ *
+ * Render lanes of the host path (1..8, default 1): lanes - 1 child contexts,
  * each with the reserved scratch and its own stream, render the views of a
  * unimgs_render_host[_async] call round-robin from the shared uploaded scene
  * (independent views overlap one view's latency-bound binning with another's
@@ -315,7 +322,9 @@ UNIMGS_API int unimgs_render_host_async(unimgs_ctx *c, const unimgs_gaussians *g
 UNIMGS_API int unimgs_set_host_lanes(unimgs_ctx *c, int32_t lanes);
 
 /* Wait for every unimgs_render_host_async call of this context (uploads,
- * renders, read-backs); UNIMGS_ERR_CAPACITY if the last frame overflowed. */
+ * renders, read-backs); UNIMGS_ERR_CAPACITY if ANY view rendered since the
+ * previous wait overflowed max_pairs (a device flag that only this call
+ * clears): the frames of that batch in out_host are then not all valid. */
 UNIMGS_API int unimgs_host_wait(unimgs_ctx *c);
 
 /* Number of kernel launches enqueued by this context since creation. */

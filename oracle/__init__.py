@@ -99,7 +99,7 @@ def lib():
         L.or_sh_basis_colour.argtypes = [vp, i32, vp, vp]
         L.or_set_cov3d.argtypes = [vp, vp]
         L.or_set_cov3d.restype = None
-        L.or_deform.argtypes = [vp, i32, vp, vp, vp, i64, vp, vp, vp, vp, vp]
+        L.or_deform.argtypes = [vp, i32, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp]
         L.or_deform.restype = i32
         L.or_rodrigues_public.argtypes = [vp, vp]
         L.or_rodrigues_public.restype = None
@@ -175,7 +175,8 @@ class Oracle:
             L.or_set_cov3d(self._h, _ptr(self._cov))
 
     def deform(self, binding, field, faces):
-        """Eq.12-13: deformed (means [N,3], covariances [N,6] xx xy xz yy yz zz) in float64."""
+        """Eq.12-13: deformed (means [N,3], covariances [N,6] xx xy xz yy yz zz) in float64.
+        V = number of per-vertex field rows; faces with a vertex id outside [0, V) are skipped."""
         face = np.ascontiguousarray(binding.face, np.int32)
         bary = np.ascontiguousarray(binding.bary, np.float32)
         fc = np.ascontiguousarray(faces, np.int32)
@@ -185,7 +186,8 @@ class Oracle:
         mu = np.zeros((self.N, 3), np.float64)
         cv = np.zeros((self.N, 6), np.float64)
         K = int(face.shape[1])
-        if lib().or_deform(self._h, K, _ptr(face), _ptr(bary), _ptr(fc), int(fc.shape[0]), _ptr(d), _ptr(lr),
+        if lib().or_deform(self._h, K, _ptr(face), _ptr(bary), _ptr(fc), int(fc.shape[0]), int(d.shape[0]),
+                           _ptr(d), _ptr(lr),
                            _ptr(sh), _ptr(mu), _ptr(cv)):
             raise ValueError("anchors per Gaussian must be 1..8")
         return mu, cv

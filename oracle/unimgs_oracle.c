@@ -950,7 +950,8 @@ static void or_rodrigues(const double w[3], double R[3][3]) {
 void or_rodrigues_public(const double *w, double *R) { or_rodrigues(w, (double(*)[3])R); }
 
 int or_deform(const or_ctx *c, int K, const int32_t *face, const float *bary, const int32_t *faces, int64_t F,
-              const float *delta, const float *log_rot, const float *shear, double *mu_out, double *cov_out) {
+              int64_t V, const float *delta, const float *log_rot, const float *shear, double *mu_out,
+              double *cov_out) {
     if (K < 1 || K > 8) return 1;
 #pragma omp parallel for schedule(static)
     for (int64_t g = 0; g < c->N; g++) {
@@ -979,6 +980,11 @@ int or_deform(const or_ctx *c, int K, const int32_t *face, const float *bary, co
         for (int i = 0; i < K; i++) {
             const int32_t f = face[g * K + i];
             if (f < 0 || f >= F) continue;
+            /* a face with a vertex id outside [0, V) is invalid input, culled as a value like an
+             * unbound anchor (SPEC S:165 error-as-value; include/unimgs.h unimgs_deform) */
+            if (faces[3 * (int64_t)f] < 0 || faces[3 * (int64_t)f] >= V || faces[3 * (int64_t)f + 1] < 0 ||
+                faces[3 * (int64_t)f + 1] >= V || faces[3 * (int64_t)f + 2] < 0 || faces[3 * (int64_t)f + 2] >= V)
+                continue;
             const float *bw = bary + 3 * (g * K + i);
             for (int j = 0; j < 3; j++) {
                 const int64_t v = faces[3 * (int64_t)f + j];

@@ -296,7 +296,10 @@ extern "C" int unimgs_preprocess(unimgs_ctx *c, const unimgs_gaussians *g, const
 
 extern "C" int unimgs_bin(unimgs_ctx *c, void *stream) {
     if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
-    if (c->stage < 1) return fail(c, UNIMGS_ERR_STATE, "bin before preprocess");
+    // exactly one bin per preprocess: only k_begin_frame (run by preprocess) resets the
+    // per-frame counters, histograms and scans the bin consumes in place
+    if (c->stage != 1)
+        return fail(c, UNIMGS_ERR_STATE, c->stage < 1 ? "bin before preprocess" : "bin twice after one preprocess");
     c->sort_mode_used = c->set.tri_depth ? 1 : c->set.sort_mode;  // per-pair triangle keys need the full sort
     c->launches += launch_bin(c->buf, c->P, c->g.N, c->m.F, c->cam, c->sort_mode_used, c->set.tri_depth,
                               (cudaStream_t)stream, c->sm_count,
@@ -346,7 +349,7 @@ extern "C" int unimgs_deform(const unimgs_gaussians *rest, const unimgs_binding 
         return UNIMGS_ERR_INVALID_ARGUMENT;
     if (reinterpret_cast<uintptr_t>(f->data) & 15) return UNIMGS_ERR_INVALID_ARGUMENT;
     DeformInput d{rest->count, rest->means, rest->quats, rest->scales, rest->cov3d, b->anchors, b->face, b->bary,
-                  f->num_faces, f->faces, reinterpret_cast<const float4 *>(f->data)};
+                  f->num_faces, f->num_vertices, f->faces, reinterpret_cast<const float4 *>(f->data)};
     launch_deform(d, means_out, cov_out, (cudaStream_t)stream);
     return cudaGetLastError() == cudaSuccess ? UNIMGS_OK : UNIMGS_ERR_CUDA;
 }
@@ -452,12 +455,28 @@ extern "C" int unimgs_render_host_async(unimgs_ctx *c, const unimgs_gaussians *g
             return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "render_host: all cameras must share one size");
     const int64_t N = gh ? gh->count : 0, F = mh ? mh->num_triangles : 0, V = mh ? mh->num_vertices : 0;
     if (N < 0 || F < 0 || V < 0) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "negative counts");
+    // every host-side check of preprocess, done before anything is enqueued
+    if (N > c->max_g || F > c->max_t || N + F > c->max_prims)
+        return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "render_host: counts above reserved");
+    if (N && (!gh->means || !gh->opacities || !gh->sh || (!gh->cov3d && (!gh->quats || !gh->scales))))
+        return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "render_host: gaussian array is NULL");
+    if (N && (gh->sh_degree < 0 || gh->sh_degree > 3)) return fail(c, UNIMGS_ERR_UNSUPPORTED, "sh_degree must be 0..3");
+    if (F && (V < 1 || !mh->positions || !mh->faces || !mh->opacity))
+        return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "render_host: mesh array is NULL");
+    if (F && mh->texture && (mh->tex_width < 1 || mh->tex_height < 1))
+        return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "texture size < 1");
+    for (int v = 0; v < n_views; v++) {
+        CamParams cp;
+        int rc = make_cam(c, &cams[v], cp);
+        if (rc) return rc;
+    }
+    const bool cov = N && gh->cov3d;  // given covariances replace quats/scales (N3)
     const int shk = N ? (gh->sh_degree + 1) * (gh->sh_degree + 1) : 0;
     const bool tex = mh && mh->texture && mh->uvs && F;
-    const size_t sz[] = {al256(N * 12), al256(N * 16), al256(N * 12), al256(N * 4), al256(N * shk * 12),
-                         al256(V * 12), al256(mh && mh->uvs ? V * 8 : 0), al256(mh && mh->colors ? V * 12 : 0),
-                         al256(F * 12), al256(F * 4),
-                         al256(tex ? (size_t)mh->tex_width * mh->tex_height * 4 : 0)};
+    const size_t sz[] = {al256(N * 12), al256(cov ? 0 : N * 16), al256(cov ? 0 : N * 12), al256(N * 4),
+                         al256(N * shk * 12), al256(V * 12), al256(mh && mh->uvs ? V * 8 : 0),
+                         al256(mh && mh->colors ? V * 12 : 0), al256(F * 12), al256(F * 4),
+                         al256(tex ? (size_t)mh->tex_width * mh->tex_height * 4 : 0), al256(cov ? N * 24 : 0)};
     size_t total = 0;
     for (size_t x : sz) total += x;
     cudaStream_t s = (cudaStream_t)stream;
@@ -507,28 +526,31 @@ extern "C" int unimgs_render_host_async(unimgs_ctx *c, const unimgs_gaussians *g
         }
     }
     char *p = (char *)c->stage_buf[slot];
-    char *dp[11];
-    for (int i = 0; i < 11; i++) { dp[i] = p; p += sz[i]; }
-    const void *src[] = {N ? gh->means : nullptr, N ? gh->quats : nullptr, N ? gh->scales : nullptr,
-                         N ? gh->opacities : nullptr, N ? gh->sh : nullptr, F ? mh->positions : nullptr,
-                         F ? mh->uvs : nullptr, F ? mh->colors : nullptr, F ? mh->faces : nullptr,
-                         F ? mh->opacity : nullptr, tex ? mh->texture : nullptr};
-    const size_t bytes[] = {(size_t)N * 12, (size_t)N * 16, (size_t)N * 12, (size_t)N * 4, (size_t)N * shk * 12,
-                            (size_t)V * 12, (mh && mh->uvs) ? (size_t)V * 8 : 0, (mh && mh->colors) ? (size_t)V * 12 : 0,
-                            (size_t)F * 12, (size_t)F * 4,
-                            tex ? (size_t)mh->tex_width * mh->tex_height * 4 : 0};
+    constexpr int kArrays = 12;
+    char *dp[kArrays];
+    for (int i = 0; i < kArrays; i++) { dp[i] = p; p += sz[i]; }
+    const void *src[] = {N ? gh->means : nullptr, cov ? nullptr : (N ? gh->quats : nullptr),
+                         cov ? nullptr : (N ? gh->scales : nullptr), N ? gh->opacities : nullptr,
+                         N ? gh->sh : nullptr, F ? mh->positions : nullptr, F ? mh->uvs : nullptr,
+                         F ? mh->colors : nullptr, F ? mh->faces : nullptr, F ? mh->opacity : nullptr,
+                         tex ? mh->texture : nullptr, cov ? gh->cov3d : nullptr};
+    const size_t bytes[] = {(size_t)N * 12, cov ? 0 : (size_t)N * 16, cov ? 0 : (size_t)N * 12, (size_t)N * 4,
+                            (size_t)N * shk * 12, (size_t)V * 12, (mh && mh->uvs) ? (size_t)V * 8 : 0,
+                            (mh && mh->colors) ? (size_t)V * 12 : 0, (size_t)F * 12, (size_t)F * 4,
+                            tex ? (size_t)mh->tex_width * mh->tex_height * 4 : 0, cov ? (size_t)N * 24 : 0};
     // upload on its own stream, once the call two back (same buffer) has rendered
     if (c->host_calls >= 2) {
         CUDA_TRY(c, cudaStreamWaitEvent(c->up_stream, c->ev_stage_free[slot], 0));
         for (int l = 1; l < c->lanes; l++) CUDA_TRY(c, cudaStreamWaitEvent(c->up_stream, c->ev_lane_free[slot][l], 0));
     }
-    for (int i = 0; i < 11; i++)
+    for (int i = 0; i < kArrays; i++)
         if (src[i] && bytes[i])
             CUDA_TRY(c, cudaMemcpyAsync(dp[i], src[i], bytes[i], cudaMemcpyHostToDevice, c->up_stream));
     CUDA_TRY(c, cudaEventRecord(c->ev_uploaded[slot], c->up_stream));
     CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_uploaded[slot], 0));
-    unimgs_gaussians gd{N, (const float *)dp[0], (const float *)dp[1], (const float *)dp[2], (const float *)dp[3],
-                        (const float *)dp[4], N ? gh->sh_degree : 0, nullptr};
+    unimgs_gaussians gd{N, (const float *)dp[0], cov ? nullptr : (const float *)dp[1],
+                        cov ? nullptr : (const float *)dp[2], (const float *)dp[3], (const float *)dp[4],
+                        N ? gh->sh_degree : 0, cov ? (const float *)dp[11] : nullptr};
     unimgs_mesh md{V, F, (const float *)dp[5], (F && mh->uvs) ? (const float *)dp[6] : nullptr,
                    (F && mh->colors) ? (const float *)dp[7] : nullptr, (const int32_t *)dp[8], (const float *)dp[9],
                    tex ? (const uint8_t *)dp[10] : nullptr, tex ? mh->tex_width : 0, tex ? mh->tex_height : 0};
@@ -544,8 +566,10 @@ extern "C" int unimgs_render_host_async(unimgs_ctx *c, const unimgs_gaussians *g
         CUDA_TRY(c, cudaStreamWaitEvent(x->bin_stream, x->ev_ready, 0));
         int rc = unimgs_preprocess(x, &gd, &md, &cams[v], x->bin_stream);
         if (!rc) rc = unimgs_bin(x, x->bin_stream);
-        if (rc) {
+        if (rc) {  // (host checks all passed above, so this is a CUDA error): drain so the
+                   // slot's next upload cannot race with the views already queued
             if (x != c) c->err = x->err;
+            cudaDeviceSynchronize();
             return rc;
         }
         CUDA_TRY(c, cudaEventRecord(x->ev_binned, x->bin_stream));
@@ -554,6 +578,7 @@ extern "C" int unimgs_render_host_async(unimgs_ctx *c, const unimgs_gaussians *g
         rc = unimgs_render(x, x->frames[bi], ls);
         if (rc) {
             if (x != c) c->err = x->err;
+            cudaDeviceSynchronize();
             return rc;
         }
         CUDA_TRY(c, cudaEventRecord(x->ev_render[bi], ls));
@@ -578,14 +603,23 @@ extern "C" int unimgs_host_wait(unimgs_ctx *c) {
     CUDA_TRY(c, cudaStreamSynchronize(c->up_stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->copy_stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->host_stream));
+    bool overflowed = false;
+    unsigned long long needed = 0;
     for (int l = 0; l < c->lanes; l++) {
         unimgs_ctx *x = l ? c->child[l] : c;
         if (l) CUDA_TRY(c, cudaStreamSynchronize(c->lane_stream[l]));
         DevState h;
         CUDA_TRY(c, cudaMemcpy(&h, x->buf.st, sizeof h, cudaMemcpyDeviceToHost));
-        if (h.overflow)
-            return fail(c, UNIMGS_ERR_CAPACITY, "capacity: %llu pairs needed", (unsigned long long)h.needed);
+        if (h.overflow_sticky) {  // any view since the last wait (begin_frame clears only `overflow`)
+            CUDA_TRY(c, cudaMemset(&x->buf.st->overflow_sticky, 0, sizeof(unsigned int)));
+            overflowed = true;
+            needed = std::max(needed, (unsigned long long)h.needed);
+        }
     }
+    if (overflowed)
+        return fail(c, UNIMGS_ERR_CAPACITY,
+                    "capacity: at least one view since the last wait overflowed (its frame is not valid); "
+                    "the last view needed %llu pairs, %lld reserved", needed, (long long)c->max_pairs);
     return UNIMGS_OK;
 }
 

@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(1024) k_scan_counts(uint32_t *cnt, int64_t n, 
             st->needed = total;
             const bool over = (int64_t)total > cap;
             st->overflow = over ? 1u : 0u;
+            if (over) st->overflow_sticky = 1u;  // survives k_begin_frame of later views (unimgs_host_wait)
             st->K = over ? 0u : total;
         }
     }

@@ -44,6 +44,10 @@ __global__ void __launch_bounds__(256) k_deform(DeformInput d, float *__restrict
         const float b3[3] = {__ldg(bw), __ldg(bw + 1), __ldg(bw + 2)};
         const int v3[3] = {__ldg(d.faces + 3 * (int64_t)f), __ldg(d.faces + 3 * (int64_t)f + 1),
                            __ldg(d.faces + 3 * (int64_t)f + 2)};
+        // a face with a vertex id outside [0, V) is junk: the anchor is skipped like an unbound one
+        if ((unsigned)v3[0] >= (unsigned long long)d.V || (unsigned)v3[1] >= (unsigned long long)d.V ||
+            (unsigned)v3[2] >= (unsigned long long)d.V)
+            continue;
 #pragma unroll
         for (int j = 0; j < 3; j++) {
             const float4 *vp = d.vdata + 3 * (int64_t)v3[j];

@@ -11,11 +11,11 @@ constexpr int kBlendThreads = 256;
 constexpr int kMaxPasses = 8;
 
 // Per-frame device counters.  frame_epoch survives across frames (it tags
-// decoupled-look-back entries so the look-back buffers never need clearing);
-// everything after it is zeroed by k_begin_frame.
+// decoupled-look-back entries so the look-back buffers never need clearing) and so
+// does overflow_sticky; everything after them is zeroed by k_begin_frame.
 struct DevState {
     unsigned int frame_epoch;
-    unsigned int pad0;
+    unsigned int overflow_sticky;  // set by any frame that overflowed; cleared only by unimgs_host_wait
     unsigned int n_vis;         // visible primitives (compacted)
     unsigned int K;             // pairs written (0 on overflow)
     unsigned long long needed;  // pairs required (saturating at 2^32-1)
@@ -92,8 +92,8 @@ struct DeformInput {
     int K;                 // anchors per Gaussian
     const int32_t *face;   // [N][K]
     const float *bary;     // [N][K][3]
-    int64_t F;
-    const int32_t *faces;  // [F][3]
+    int64_t F, V;
+    const int32_t *faces;  // [F][3], vertex ids checked against [0, V)
     const float4 *vdata;   // per vertex 3 x float4: delta xyz + log_rot x | log_rot yz + shear xx xy | shear xz yy yz zz
 };
 
