@@ -19,14 +19,10 @@
 //   its pixels have stopped.
 //   out = (C + T bg_alpha bg, T) with the exit T of an open entity (R3, R5).
 // Triangle colour: perspective-correct barycentrics at the pixel centre in
-// fp64 (lambda_k ~ E_k z_i z_j, exact products), manual fp32 bilinear texture.
+// fp32 (w_k = E_k z_i z_j), manual fp32 bilinear texture (colour tolerance 1e-3).
 #include "internal.cuh"
 
 namespace unimgs {
-
-#ifndef UNIMGS_BLEND_PIX
-#define UNIMGS_BLEND_PIX 1
-#endif
 
 struct TexView {
     const uchar4 *tex;
@@ -166,6 +162,12 @@ __device__ __forceinline__ bool tri_touches(const float4 &a, const float4 &b, in
     return mxx >= Rx0 && mnx <= Rx0 + 256 * 8 - 1 && mxy >= Ry0 && mny <= Ry1;
 }
 
+__device__ __forceinline__ float lg2_ftz(float x) {  // x = o >= 1/255: never subnormal
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float ex2_ftz(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -176,18 +178,23 @@ __device__ __forceinline__ float ex2_ftz(float x) {
 enum { MODE_EXACT = 0, MODE_NAIVE = 1, MODE_MSAA_PIXEL = 2, MODE_WHOLE_PIXEL = 3, MODE_PAPER_LITERAL = 4 };
 
 // Per-pixel blend state (registers).  G / Tl only exist for the modes that use them.
+// While an entity is open, T holds its exit transmittance (R3: refreshed by every
+// triangle) and Tlast a copy of it: any Gaussian fragment (alpha >= 1/255) lowers T,
+// so "the entity is still open" is exactly T == Tlast and the Gaussian path keeps
+// no entity state at all.  (T == 0 would stay "open", which changes nothing: every
+// later contribution is then 0 either way.)  The whole-pixel ablation mode, whose
+// Gaussians do not close the entity, keeps an explicit flag.  A finished pixel is
+// marked by py = NaN: its Gaussian test q <= q_max then fails by itself.
 template <int MODE, int M>
 struct Px {
     float C0, C1, C2, T, Te;
     float t[M];
     float G, Tl;
-    float Tx;  // cached exit transmittance of the open entity (refreshed by each triangle)
-    float py;  // pixel centre y for the Gaussian test; NaN once done (the test then fails by itself)
-    bool open, done;
-    __device__ __forceinline__ void finish() {
-        done = true;
-        py = __int_as_float(0x7fc00000);
-    }
+    float Tlast;  // T after the last triangle fragment (NaN: none yet)
+    float py;     // pixel centre y for the Gaussian test; NaN once done
+    bool open;    // MODE_WHOLE_PIXEL only
+    __device__ __forceinline__ bool done() const { return py != py; }
+    __device__ __forceinline__ void finish() { py = __int_as_float(0x7fc00000); }
     __device__ __forceinline__ float mean_t() const {
         float a = 0.f;
 #pragma unroll
@@ -237,7 +244,8 @@ __device__ __forceinline__ void tri_pixel(Px<MODE, M> &s, const int X[3], const 
         if (s.T < t_eps) s.finish();
         return;
     }
-    if (!s.open) {
+    const bool open = MODE == MODE_WHOLE_PIXEL ? s.open : s.T == s.Tlast;
+    if (!open) {
         s.open = true;
         s.Te = s.T;
         s.G = 1.f;
@@ -256,24 +264,67 @@ __device__ __forceinline__ void tri_pixel(Px<MODE, M> &s, const int X[3], const 
     for (int j = 0; j < M; j++)
         if ((m >> j) & 1u) s.t[j] *= kk;  // Eq.7
     if (MODE == MODE_PAPER_LITERAL) s.Tl *= 1.f - popc_frac<M>(m) * al;
-    s.Tx = s.exit_T();
-    if (s.Tx < t_eps) s.finish();
+    s.T = s.exit_T();  // T_eff (and the T a closing Gaussian continues from)
+    s.Tlast = s.T;
+    if (s.T < t_eps) s.finish();
 }
 
-// One CTA per 16x16 tile, independent warps, PIX pixels per lane (vertically
-// 4 rows apart).  Warp w owns an 8 x (4 PIX) sub-tile.  Each warp walks the
-// whole tile list in chunks of 32 (lane l holds entry 32c + l; ids are
-// prefetched two chunks ahead and records one chunk ahead), keeps the entries
-// that touch its sub-tile (ballot), packs them into its own shared buffer and
-// blends them in list order with broadcast reads.  No block-wide barrier: a
-// warp stops as soon as all of its pixels have terminated.  A packed triangle
-// entry carries q_max = -1, so the Gaussian membership test rejects it for
-// free and only the (rare) miss path checks for triangles.
+// Packed f32x2 arithmetic (sm_100: FADD2 / FMUL2 / FFMA2, one issue slot for two
+// IEEE round-to-nearest fp32 operations -- per element identical to __fadd_rn etc.,
+// so N6 stays bit-exact).  The pair lives in one 64-bit register.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void upk2(f32x2 r, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// Per-warp packed entry buffer.  Entries 2p and 2p+1 form pair p, stored
+// structure-of-arrays so that one 16-byte shared load yields f32x2 operands:
+//   e[p][0] = {u0, u1, v0, v1}        (triangle: X0, Y0 bits)
+//   e[p][1] = {ca0, ca1, cc0, cc1}    (triangle: X1, Y1 bits)
+//   e[p][2] = {2cb0, 2cb1, qm0, qm1}  (triangle: X2 bits, q_max = -1; padding: NaN)
+//   col[k]  = {r, g, b, log2 o}       (triangle: Y2 bits, kind, alpha, id)
+struct WarpBuf {
+    float4 e[16][3];
+    float4 col[32];
+};
+
+// One CTA per 16x16 tile, 8 independent warps, one pixel per lane.  Warp w owns
+// the 8x4 sub-tile (w & 1, w >> 1) and walks the whole tile list in chunks of 32
+// entries (lane l <-> entry 32c + l):
+//   1. the chunk's records (48 B per Gaussian, the first 32 B per triangle) were
+//      copied by cp.async into the warp's stage while the previous chunk was
+//      blended (ids are prefetched one chunk further ahead, in registers);
+//   2. each lane culls its entry exactly against the warp's sub-tile, a ballot
+//      ranks the survivors, which are packed into the warp's pair buffer;
+//   3. the next chunk's records are requested (cp.async, no registers held);
+//   4. the packed entries are tested four at a time (two f32x2 pairs) and the
+//      hits blended in list order.
+// No block-wide barrier: a warp stops as soon as all of its pixels have terminated.
 #ifndef UNIMGS_BLEND_MINB
-#define UNIMGS_BLEND_MINB (4 * PIX)
+#define UNIMGS_BLEND_MINB 4
 #endif
-template <bool COUNT, int PIX, int MODE, int M>
-__global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blend(const uint2 *__restrict__ ranges,
+template <bool COUNT, int MODE, int M>
+__global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(const uint2 *__restrict__ ranges,
                                                                      const uint32_t *__restrict__ order,
                                                                      const uint32_t *__restrict__ vals,
                                                                      const GaussRecord *__restrict__ grec,
@@ -282,175 +333,213 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
                                                                      BlendParams bp, float4 *__restrict__ out,
                                                                      DevState *st) {
     if (st->overflow) return;
-    constexpr int NW = kBlendThreads / PIX / 32;  // warps per tile
+    constexpr int NW = kBlendThreads / 32;  // warps per tile
     unsigned long long w_gt = 0, w_gf = 0, w_tt = 0, w_tf = 0;  // COUNT only
-    __shared__ float4 s_buf[NW][32][3];  // per-warp packed entries: a (u, v, q_max, o), (ca, 2cb, cc, id), c
-    __shared__ TriAttr s_tri[NW][32];    // a packed triangle entry's q2..q5 (cp.async)
+    __shared__ WarpBuf s_buf[NW];
+    __shared__ float4 s_stage[NW][32][3];  // this lane's record of the next chunk (cp.async)
+    __shared__ TriAttr s_tri[NW][32];      // a packed triangle entry's q2..q5 (cp.async)
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = (int)__ldg(order + blockIdx.x);  // longest-first schedule (k_tile_order)
     const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int sx0 = tx * kTile + (warp & 1) * 8, sy0 = ty * kTile + (warp >> 1) * 4 * PIX;
-    const int x = sx0 + (lane & 7), y0 = sy0 + (lane >> 3);
+    const int sx0 = tx * kTile + (warp & 1) * 8, sy0 = ty * kTile + (warp >> 1) * 4;
+    const int x = sx0 + (lane & 7), y = sy0 + (lane >> 3);
     const float px = (float)x + 0.5f;
-    const float rx0 = (float)sx0 + 0.5f, ry0 = (float)sy0 + 0.5f, ry1 = ry0 + (float)(4 * PIX - 1);
-    const int Rx0 = 256 * sx0, Ry0 = 256 * sy0, Ry1 = 256 * (sy0 + 4 * PIX) - 1;
+    const float rx0 = (float)sx0 + 0.5f, ry0 = (float)sy0 + 0.5f, ry1 = ry0 + 3.f;
+    const int Rx0 = 256 * sx0, Ry0 = 256 * sy0, Ry1 = 256 * (sy0 + 4) - 1;
     const uint2 rg = ranges[tile];
     const unsigned lt = (1u << lane) - 1u;
-    float4(*buf)[3] = s_buf[warp];
+    WarpBuf &wb = s_buf[warp];
+    float *ef = &wb.e[0][0].x;
     TriAttr *tat = s_tri[warp];
+    float4 *stg = s_stage[warp][lane];
+    const unsigned stg_s = (unsigned)__cvta_generic_to_shared(stg);
 
-    Px<MODE, M> s[PIX];
+    Px<MODE, M> s;
+    s.C0 = s.C1 = s.C2 = 0.f;
+    s.T = s.Te = s.G = s.Tl = 1.f;
 #pragma unroll
-    for (int p = 0; p < PIX; p++) {
-        s[p].C0 = s[p].C1 = s[p].C2 = 0.f;
-        s[p].T = s[p].Te = s[p].G = s[p].Tl = s[p].Tx = 1.f;
-#pragma unroll
-        for (int j = 0; j < M; j++) s[p].t[j] = 1.f;
-        s[p].open = false;
-        s[p].done = false;
-        s[p].py = (float)(y0 + 4 * p) + 0.5f;
-        if (!(x < W && y0 + 4 * p < H)) s[p].finish();
-    }
-    auto all_done = [&]() {
-        bool d = true;
-#pragma unroll
-        for (int p = 0; p < PIX; p++) d = d && s[p].done;
-        return d;
-    };
+    for (int j = 0; j < M; j++) s.t[j] = 1.f;
+    s.open = false;
+    s.Tlast = __int_as_float(0x7fc00000);
+    s.py = (float)y + 0.5f;
+    if (!(x < W && y < H)) s.finish();
 
-    // ids two chunks ahead, records one chunk ahead
-    unsigned id1 = rg.x + lane < rg.y ? __ldg(vals + rg.x + lane) : 0xFFFFFFFFu;
-    unsigned id2 = rg.x + 32 + lane < rg.y ? __ldg(vals + rg.x + 32 + lane) : 0xFFFFFFFFu;
-    float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na, nc = na;
-    auto fetch_rec = [&](unsigned id) {
-        if (id == 0xFFFFFFFFu) return;
-        if (id >= F) {
-            const GaussRecord *g = grec + (id - F);
-            na = __ldg(&g->a); nb = __ldg(&g->b); nc = __ldg(&g->c);
-        } else {
-            const int4 *q = reinterpret_cast<const int4 *>(trec + id);
-            const int4 q0 = __ldg(q), q1 = __ldg(q + 1);
-            na = make_float4(__int_as_float(q0.x), __int_as_float(q0.y), __int_as_float(q0.z), __int_as_float(q0.w));
-            nb = make_float4(__int_as_float(q1.x), __int_as_float(q1.y), __int_as_float(q1.z), __int_as_float(q1.w));
+    // cp.async of entry id's record into this lane's stage slot (Gaussian 48 B,
+    // triangle q0/q1 32 B); always commits one group
+    auto stage_rec = [&](unsigned id) {
+        if (id != 0xFFFFFFFFu) {
+            const char *src = id >= F ? reinterpret_cast<const char *>(grec + (id - F))
+                                      : reinterpret_cast<const char *>(trec + id);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(stg_s), "l"(src) : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(stg_s + 16), "l"(src + 16) : "memory");
+            if (id >= F)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(stg_s + 32), "l"(src + 32) : "memory");
         }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    fetch_rec(id1);
+    unsigned id0 = rg.x + lane < rg.y ? __ldg(vals + rg.x + lane) : 0xFFFFFFFFu;
+    unsigned id1 = rg.x + 32 + lane < rg.y ? __ldg(vals + rg.x + 32 + lane) : 0xFFFFFFFFu;
+    stage_rec(id0);
     const float kexp = -0.72134752044448170f;  // -log2(e) / 2
 
+    // Eq.1-2 blend of Gaussian fragment k (membership already decided bit-exactly):
+    // alpha = min(alpha_max, o e^{-q/2}) = min(alpha_max, 2^(q kexp + log2 o))
+    auto gblend = [&](float q, unsigned k) {
+        if (COUNT) w_gf++;
+        const float4 ec = wb.col[k];
+        const float al = fminf(bp.alpha_max, ex2_ftz(fmaf(q, kexp, ec.w)));
+        if (MODE == MODE_WHOLE_PIXEL && s.open) {
+            // Fig.3b/c: the entity spans the whole list; the Gaussian does not
+            // attenuate its sub-pixel state (colour overflow)
+            const float base = s.Te * s.mean_t();
+            const float w = base * s.G * al;
+            s.C0 += w * ec.x; s.C1 += w * ec.y; s.C2 += w * ec.z;
+            s.G *= 1.f - al;
+            if (base * s.G < bp.t_eps) s.finish();
+            return;
+        }
+        // depth adjacency broken: T already holds the entity's exit T (R3),
+        // and lowering it closes the entity (T != Tlast)
+        const float w = s.T * al;
+        s.C0 += w * ec.x; s.C1 += w * ec.y; s.C2 += w * ec.z;
+        s.T -= w;
+        if (s.T < bp.t_eps) s.finish();
+    };
+    // N6 for the two entries of pair p at this lane's pixel:
+    //   dx = (x + .5) - u; dy = (y + .5) - v; q = fma(ca, dx dx, fma(cc, dy dy, 2cb (dx dy)))
+    // (py is NaN once the pixel is done, so its q is NaN and no test passes)
+    auto qpair = [&](unsigned p, float &q0, float &q1, float &m0, float &m1) {
+        const float4 A = wb.e[p][0], B = wb.e[p][1], Cc = wb.e[p][2];
+        const f32x2 dx = sub2(pk2(px, px), pk2(A.x, A.y));
+        const f32x2 dy = sub2(pk2(s.py, s.py), pk2(A.z, A.w));
+        const f32x2 t = fma2(pk2(B.z, B.w), mul2(dy, dy), mul2(pk2(Cc.x, Cc.y), mul2(dx, dy)));
+        upk2(fma2(pk2(B.x, B.y), mul2(dx, dx), t), q0, q1);
+        m0 = Cc.z;
+        m1 = Cc.w;
+    };
+
     for (unsigned base = rg.x; base < rg.y; base += 32) {
-        if (__all_sync(0xffffffffu, all_done())) break;
-        const unsigned id = id1;
-        const float4 a = na, b = nb, c = nc;
-        id1 = id2;
-        id2 = base + 64 + lane < rg.y ? __ldg(vals + base + 64 + lane) : 0xFFFFFFFFu;
-        fetch_rec(id1);
+        if (__all_sync(0xffffffffu, s.done())) break;
+        const unsigned id = id0;
+        id0 = id1;
+        id1 = base + 64 + lane < rg.y ? __ldg(vals + base + 64 + lane) : 0xFFFFFFFFu;
+        asm volatile("cp.async.wait_all;\n" ::: "memory");  // this chunk's records (own slot only)
         bool rel = false;
-        if (id != 0xFFFFFFFFu)
-            rel = id >= F ? gauss_touches(a, b, c, rx0, ry0, ry1) : tri_touches(a, b, Rx0, Ry0, Ry1);
+        float4 a, b, c;
+        if (id != 0xFFFFFFFFu) {
+            a = stg[0];
+            b = stg[1];
+            if (id >= F) {
+                c = stg[2];
+                rel = gauss_touches(a, b, c, rx0, ry0, ry1);
+            } else {
+                rel = tri_touches(a, b, Rx0, Ry0, Ry1);
+            }
+        }
         const unsigned bal = __ballot_sync(0xffffffffu, rel);
         const bool has_tri = __any_sync(0xffffffffu, rel && id < F);
+        const unsigned cnt = __popc(bal);
+        const unsigned slot = __popc(bal & lt);
         if (rel) {
-            const unsigned slot = __popc(bal & lt);
+            float *e = ef + 12 * (slot >> 1) + (slot & 1);
             if (id >= F) {
-                buf[slot][0] = a;
-                buf[slot][1] = make_float4(b.x, b.y + b.y, b.z, __uint_as_float(id));
-                buf[slot][2] = c;
+                e[0] = a.x; e[2] = a.y; e[4] = b.x; e[6] = b.z; e[8] = b.y + b.y; e[10] = a.z;
+                wb.col[slot] = make_float4(c.x, c.y, c.z, lg2_ftz(a.w));
             } else {
-                // triangle: q_max = -1 (no Gaussian test passes), the prefetched vertices,
-                // kind and alpha staged with it: (X0, Y0, -1, Y1), (X2, Y2, X1, id), (kind, alpha)
-                buf[slot][0] = make_float4(a.x, a.y, -1.f, a.w);
-                buf[slot][1] = make_float4(b.x, b.y, a.z, __uint_as_float(id));
-                buf[slot][2] = make_float4(b.z, b.w, 0.f, 0.f);
+                // triangle: the staged vertices, kind and alpha; q_max = -1 marks it
+                e[0] = a.x; e[2] = a.y; e[4] = a.z; e[6] = a.w; e[8] = b.x; e[10] = -1.f;
+                wb.col[slot] = make_float4(b.y, b.z, b.w, __uint_as_float(id));
                 const char *src = reinterpret_cast<const char *>(&trec[id].q2);
                 const unsigned dst = (unsigned)__cvta_generic_to_shared(&tat[slot]);
 #pragma unroll
                 for (int w = 0; w < 4; w++)
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * w), "l"(src + 16 * w)
                                  : "memory");
-                asm volatile("cp.async.commit_group;\n" ::: "memory");
             }
         }
-        __syncwarp();
-        const unsigned cnt = __popc(bal);
-        // Gaussian fragment test + blend (Eq.1-2) of packed entry k for each pixel
-        auto gauss = [&](const float4 &ea, const float4 &eb, unsigned k) {
-            const float dx = __fsub_rn(px, ea.x);
-            const float dxx = __fmul_rn(dx, dx);
-            bool hit[PIX], any = false;
-            float q[PIX];
+        asm volatile("cp.async.commit_group;\n" ::: "memory");  // this chunk's triangle attributes
+        // padding up to a multiple of 4 entries: q_max = NaN fails every test, and a
+        // zero colour keeps the predicated blend's 0 * colour finite
+        const unsigned cnt4 = (cnt + 3) & ~3u;
+        if (lane >= cnt && lane < cnt4) {
+            ef[12 * (lane >> 1) + 10 + (lane & 1)] = __int_as_float(0x7fc00000);
+            wb.col[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncwarp();  // packing done, the stage slot is free again
+        stage_rec(id0);  // next chunk's records land while this one is blended
+        if (!has_tri && MODE != MODE_WHOLE_PIXEL) {
+            // Gaussian-only chunk: four entries per iteration.  Membership of all four by
+            // two f32x2 pairs, their alphas computed unconditionally (independent chains),
+            // then Eq.1-2 as a predicated sequence: entry k blends iff it is a fragment
+            // and the pixel has not terminated (T >= t_eps) -- blend-then-test, R16.
+#pragma unroll 1
+            for (unsigned p = 0; 2 * p < cnt; p += 2) {
+                float q[4], m[4];
+                qpair(p, q[0], q[1], m[0], m[1]);
+                qpair(p + 1, q[2], q[3], m[2], m[3]);
+                if (COUNT && !s.done()) w_gt += min(4u, cnt - 2 * p);
+                float4 ec[4];
+                float al[4];
 #pragma unroll
-            for (int p = 0; p < PIX; p++) {
-                const float dy = __fsub_rn(s[p].py, ea.y);
-                q[p] = __fmaf_rn(eb.x, dxx, __fmaf_rn(eb.z, __fmul_rn(dy, dy), __fmul_rn(eb.y, __fmul_rn(dx, dy))));
-                hit[p] = q[p] <= ea.z;  // false once done: py is NaN
-                if (COUNT && ea.z >= 0.f && !s[p].done) w_gt++;
-                any = any || hit[p];
-            }
-            if (!any) return false;
-            const float4 ec = buf[k][2];
+                for (int k = 0; k < 4; k++) {
+                    ec[k] = wb.col[2 * p + k];
+                    al[k] = fminf(bp.alpha_max, ex2_ftz(fmaf(q[k], kexp, ec[k].w)));
+                }
 #pragma unroll
-            for (int p = 0; p < PIX; p++) {
-                if (!hit[p]) continue;
-                if (COUNT) w_gf++;
-                const float al = fminf(bp.alpha_max, ea.w * ex2_ftz(q[p] * kexp));
-                if (MODE == MODE_WHOLE_PIXEL && s[p].open) {
-                    // Fig.3b/c: the entity spans the whole list; the Gaussian does not
-                    // attenuate its sub-pixel state (colour overflow)
-                    const float base = s[p].Te * s[p].mean_t();
-                    const float w = base * s[p].G * al;
-                    s[p].C0 += w * ec.x; s[p].C1 += w * ec.y; s[p].C2 += w * ec.z;
-                    s[p].G *= 1.f - al;
-                    if (base * s[p].G < bp.t_eps) s[p].finish();
-                    continue;
+                for (int k = 0; k < 4; k++) {
+                    // (entry 0: a pixel already done has q = NaN, so no T test is needed)
+                    const bool h = q[k] <= m[k] && (k == 0 || s.T >= bp.t_eps);
+                    const float w = h ? s.T * al[k] : 0.f;
+                    s.C0 += w * ec[k].x; s.C1 += w * ec[k].y; s.C2 += w * ec[k].z;
+                    s.T -= w;  // a fragment closes an open entity: T != Tlast
+                    if (COUNT && h) w_gf++;
                 }
-                if (MODE != MODE_NAIVE && MODE != MODE_MSAA_PIXEL && s[p].open) {
-                    s[p].T = s[p].Tx;  // depth adjacency broken: exit T (R3)
-                    s[p].open = false;
-                }
-                const float w = s[p].T * al;
-                s[p].C0 += w * ec.x; s[p].C1 += w * ec.y; s[p].C2 += w * ec.z;
-                s[p].T -= w;
-                if (s[p].T < bp.t_eps) s[p].finish();
+                if (s.T < bp.t_eps) s.finish();
             }
-            return true;
-        };
-        if (!has_tri) {
-            // Gaussian-only chunk: two entries per iteration (independent q chains)
-            unsigned k = 0;
-            for (; k + 2 <= cnt; k += 2) {
-                const float4 ea0 = buf[k][0], eb0 = buf[k][1], ea1 = buf[k + 1][0], eb1 = buf[k + 1][1];
-                gauss(ea0, eb0, k);
-                gauss(ea1, eb1, k + 1);
+        } else if (!has_tri) {
+            // (whole-pixel ablation mode: the Gaussian update depends on the open entity)
+#pragma unroll 1
+            for (unsigned p = 0; 2 * p < cnt; p += 2) {
+                float q0, q1, q2, q3, m0, m1, m2, m3;
+                qpair(p, q0, q1, m0, m1);
+                qpair(p + 1, q2, q3, m2, m3);
+                if (COUNT && !s.done()) w_gt += min(4u, cnt - 2 * p);
+                const bool h1 = q1 <= m1, h2 = q2 <= m2, h3 = q3 <= m3;
+                if (q0 <= m0) gblend(q0, 2 * p);
+                if (h1 && !s.done()) gblend(q1, 2 * p + 1);
+                if (h2 && !s.done()) gblend(q2, 2 * p + 2);
+                if (h3 && !s.done()) gblend(q3, 2 * p + 3);
             }
-            if (k < cnt) gauss(buf[k][0], buf[k][1], k);
         } else {
-            bool staged = false;
-            for (unsigned k = 0; k < cnt; k++) {
-                const float4 ea = buf[k][0];
-                const float4 eb = buf[k][1];
-                if (ea.z >= 0.f) {  // warp-uniform: entry k is the same for every lane
-                    gauss(ea, eb, k);
-                } else {
-                    if (!staged) {  // the chunk's triangle attributes, waited for once
-                        asm volatile("cp.async.wait_all;\n" ::: "memory");
-                        __syncwarp();
-                        staged = true;
-                    }
-                    const float4 ec = buf[k][2];
-                    const int X[3] = {__float_as_int(ea.x), __float_as_int(eb.z), __float_as_int(eb.x)};
-                    const int Y[3] = {__float_as_int(ea.y), __float_as_int(ea.w), __float_as_int(eb.y)};
-                    const TriAttr &r = tat[k];
+            // a chunk holding a triangle: entries one by one, in list order
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // triangle attributes (not the next records)
+            __syncwarp();
+            for (unsigned p = 0; 2 * p < cnt; p++) {
+                float q[2], m[2];
+                qpair(p, q[0], q[1], m[0], m[1]);
 #pragma unroll
-                    for (int p = 0; p < PIX; p++)
-                        if (!s[p].done)
-                            tri_pixel<COUNT, MODE, M>(s[p], X, Y, __float_as_int(ec.x), ec.y, r, x, y0 + 4 * p, tv,
-                                                      bp.t_eps, w_tt, w_tf);
+                for (int j = 0; j < 2; j++) {
+                    const unsigned k = 2 * p + j;
+                    if (k >= cnt) break;
+                    if (m[j] >= 0.f) {  // warp-uniform: entry k is the same for every lane
+                        if (COUNT && !s.done()) w_gt++;
+                        if (q[j] <= m[j] && !s.done()) gblend(q[j], k);
+                        continue;
+                    }
+                    const float *e = ef + 12 * p + j;
+                    const float4 ec = wb.col[k];
+                    const int X[3] = {__float_as_int(e[0]), __float_as_int(e[4]), __float_as_int(e[8])};
+                    const int Y[3] = {__float_as_int(e[2]), __float_as_int(e[6]), __float_as_int(ec.x)};
+                    if (!s.done())
+                        tri_pixel<COUNT, MODE, M>(s, X, Y, __float_as_int(ec.y), ec.z, tat[k], x, y, tv, bp.t_eps,
+                                                  w_tt, w_tf);
                 }
             }
         }
         __syncwarp();
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");  // no copy may outlive the CTA's shared memory
     if (COUNT) {
         unsigned long long v[4] = {w_gt, w_gf, w_tt, w_tf};
 #pragma unroll
@@ -461,30 +550,24 @@ __global__ void __launch_bounds__(kBlendThreads / PIX, UNIMGS_BLEND_MINB) k_blen
             if (lane == 0 && xs) atomicAdd(&st->work[k], xs);
         }
     }
-#pragma unroll
-    for (int p = 0; p < PIX; p++) {
-        const int y = y0 + 4 * p;
-        if (x < W && y < H) {
-            float T = s[p].T;
-            if (s[p].open) T = s[p].exit_T();
-            const float sb = T * bp.bg_alpha;
-            out[(size_t)y * W + x] = make_float4(s[p].C0 + sb * bp.bg[0], s[p].C1 + sb * bp.bg[1], s[p].C2 + sb * bp.bg[2], T);
-        }
+    if (x < W && y < H) {
+        const float T = (MODE == MODE_WHOLE_PIXEL && s.open) ? s.exit_T() : s.T;
+        const float sb = T * bp.bg_alpha;
+        out[(size_t)y * W + x] = make_float4(s.C0 + sb * bp.bg[0], s.C1 + sb * bp.bg[1], s.C2 + sb * bp.bg[2], T);
     }
 }
 
 template <int MODE, int M>
 static void launch_mode(const Buffers &b, const MeshInput &m, const CamParams &cam, const BlendParams &bp, float *out,
                         cudaStream_t s, bool count_work) {
-    constexpr int PIX = UNIMGS_BLEND_PIX;
     const int tiles = cam.tiles_x * cam.tiles_y;
     TexView tv{reinterpret_cast<const uchar4 *>(m.tex), m.tw, m.th};
     if (count_work)
-        k_blend<true, PIX, MODE, M><<<tiles, kBlendThreads / PIX, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
+        k_blend<true, MODE, M><<<tiles, kBlendThreads, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
                                                                         (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
                                                                         reinterpret_cast<float4 *>(out), b.st);
     else
-        k_blend<false, PIX, MODE, M><<<tiles, kBlendThreads / PIX, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
+        k_blend<false, MODE, M><<<tiles, kBlendThreads, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
                                                                          (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
                                                                          reinterpret_cast<float4 *>(out), b.st);
 }

@@ -52,8 +52,8 @@ def main():
     rep = sys.argv[1]
     rows = raw(rep)
     out = []
-    print(f"| kernel | us | DRAM MB (r+w) | DRAM % | warps active % | issue % | regs | top stalls (warps/issue) |")
-    print("|---|---|---|---|---|---|---|---|")
+    print(f"| kernel | us | DRAM MB (r+w) | DRAM % | warps active % | issue % | regs | warp-inst (M) | top stalls (warps/issue) |")
+    print("|---|---|---|---|---|---|---|---|---|")
     for d in rows:
         name = d.get("Kernel Name", "?").split("(")[0].replace("void ", "")
         us = fnum(d["gpu__time_duration.sum"]) / (1e3 if fnum(d["gpu__time_duration.sum"]) > 1e4 else 1)
@@ -63,7 +63,7 @@ def main():
         top = ", ".join(f"{s} {v:.2f}" for v, s in st if v == v)
         print(f"| {name} | {d['gpu__time_duration.sum']} | {mb:.1f} | {d['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']} | "
               f"{d['sm__warps_active.avg.pct_of_peak_sustained_active']} | {d['sm__inst_issued.avg.pct_of_peak_sustained_active']} | "
-              f"{d['launch__registers_per_thread']} | {top} |")
+              f"{d['launch__registers_per_thread']} | {fnum(d['smsp__inst_executed.sum']) / 1e6:.1f} | {top} |")
         out.append({"kernel": name, **{k: d.get(k) for k in METRICS},
                     "stalls": {s: v for v, s in st}})
     if "--json" in sys.argv:
