@@ -265,6 +265,16 @@ UNIMGS_API int unimgs_bind(const unimgs_gaussians *g, const unimgs_mesh *m, cons
  * pixels up to each pixel's termination.  Synchronises `stream`. */
 UNIMGS_API int unimgs_render_counted(unimgs_ctx *c, float *out_rgbt, int64_t *work, void *stream);
 
+/* Debug variant of unimgs_render (the counting kernel): identical out_rgbt, plus
+ * per pixel counts [height][width][4] uint32 (device): {Gaussian fragments
+ * blended, triangle fragments blended, unified id of the last fragment blended
+ * (0xFFFFFFFF = none), Gaussian list entries tested}, each up to the pixel's
+ * termination (T_eff < t_eps; with t_eps = 0 every fragment of the pixel).  A
+ * fragment is a Gaussian with q <= q_max (N6, alpha >= 1/255) or a
+ * triangle with a non-zero coverage mask ("fragments overlapping the
+ * pixel"), so these counts check fragment membership bit for bit.  Async. */
+UNIMGS_API int unimgs_render_fragments(unimgs_ctx *c, float *out_rgbt, uint32_t *counts, void *stream);
+
 /* Synchronise `stream` and report the last frame's counters (host *out). */
 UNIMGS_API int unimgs_get_stats(unimgs_ctx *c, unimgs_stats *out, void *stream);
 

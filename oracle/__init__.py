@@ -75,6 +75,8 @@ def lib():
         L.or_bin.restype = i64
         L.or_render.argtypes = [vp, vp, vp, i64, i32]
         L.or_render.restype = i32
+        L.or_render_counts.argtypes = [vp, vp, vp, i64, i32]
+        L.or_render_counts.restype = i32
         L.or_render_bruteforce.argtypes = [vp, vp, i32]
         L.or_render_bruteforce.restype = i32
         L.or_pixel_fragments.argtypes = [vp, i32, i32, vp, i64]
@@ -253,6 +255,16 @@ class Oracle:
         rc = lib().or_render(self._h, _ptr(out), _ptr(tl), 0 if tl is None else len(tl), self.threads)
         if rc:
             raise RuntimeError("oracle render before bin()")
+        return out
+
+    def fragment_counts(self, tiles: Optional[Sequence[int]] = None) -> np.ndarray:
+        """Per pixel [H, W, 4] uint32: Gaussian fragments blended, triangle fragments blended,
+        id of the last fragment blended (0xFFFFFFFF none), 0 -- over the listed tiles (others 0)."""
+        H, W = self.cam.height, self.cam.width
+        out = np.zeros((H, W, 4), np.uint32)
+        tl = None if tiles is None else np.ascontiguousarray(tiles, np.int32)
+        if lib().or_render_counts(self._h, _ptr(out), _ptr(tl), 0 if tl is None else len(tl), self.threads):
+            raise RuntimeError("oracle counts before bin()")
         return out
 
     def render_bruteforce(self) -> np.ndarray:

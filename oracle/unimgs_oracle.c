@@ -753,6 +753,51 @@ static void render_pixel_tiled(const or_ctx *c, int x, int y, double out[4]) {
     pix_finish(&s, &c->set, out);
 }
 
+/* Fragment bookkeeping of the tiled render (C.1 membership, R16 termination):
+ * per pixel {Gaussian fragments blended, triangle fragments blended, unified id of
+ * the last fragment blended (0xFFFFFFFF: none), 0}, over the listed tiles (all if
+ * tiles == NULL) into out[H][W][4].  With t_eps = 0 these are all fragments of
+ * the pixel (nothing terminates).                                              */
+static void count_pixel_tiled(const or_ctx *c, int x, int y, uint32_t out[4]) {
+    int tile = (y / OR_TILE) * c->tiles_x + (x / OR_TILE);
+    uint32_t b = c->ranges[2 * tile], e = c->ranges[2 * tile + 1];
+    or_pix s;
+    pix_init(&s, &c->set);
+    or_frag fr;
+    out[0] = out[1] = out[3] = 0;
+    out[2] = 0xFFFFFFFFu;
+    for (uint32_t i = b; i < e && !s.done; i++) {
+        uint32_t p = c->vals[i];
+        int hit = (int64_t)p < c->F ? triangle_fragment(c, p, x, y, &fr)
+                                    : gaussian_fragment(c, (int64_t)p - c->F, x, y, &fr);
+        if (!hit) continue;
+        pix_apply(&s, &fr, &c->set);
+        out[fr.kind == 0 ? 0 : 1]++;
+        out[2] = p;
+    }
+}
+
+int or_render_counts(const or_ctx *c, uint32_t *out, const int32_t *tiles, int64_t n_tiles, int nthreads) {
+    if (!c->ranges) return 1;
+    int64_t T = (int64_t)c->tiles_x * c->tiles_y;
+    if (!tiles) n_tiles = T;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t ti = 0; ti < n_tiles; ti++) {
+        int64_t tile = tiles ? tiles[ti] : ti;
+        if (tile < 0 || tile >= T) continue;
+        int tx = (int)(tile % c->tiles_x), ty = (int)(tile / c->tiles_x);
+        for (int y = ty * OR_TILE; y < (ty + 1) * OR_TILE && y < c->cam.height; y++)
+            for (int x = tx * OR_TILE; x < (tx + 1) * OR_TILE && x < c->cam.width; x++)
+                count_pixel_tiled(c, x, y, out + 4 * ((int64_t)y * c->cam.width + x));
+    }
+    return 0;
+}
+
 /* Render the listed tiles (all tiles if tiles == NULL) into out[H][W][4]. */
 int or_render(or_ctx *c, double *out, const int32_t *tiles, int64_t n_tiles, int nthreads) {
     if (!c->ranges) return 1;

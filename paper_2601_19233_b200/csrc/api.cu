@@ -338,6 +338,17 @@ extern "C" int unimgs_render_counted(unimgs_ctx *c, float *out, int64_t *work_ho
     return UNIMGS_OK;
 }
 
+extern "C" int unimgs_render_fragments(unimgs_ctx *c, float *out, uint32_t *counts, void *stream) {
+    if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (c->stage < 2) return fail(c, UNIMGS_ERR_STATE, "render before bin");
+    if (!out || !counts) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "out/counts is NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    BlendParams bp{c->set.alpha_max, c->set.t_eps, c->set.bg_alpha, {c->set.bg[0], c->set.bg[1], c->set.bg[2]},
+                   c->set.blend_mode, c->set.msaa_samples};
+    c->launches += launch_blend(c->buf, c->g, c->m, c->cam, bp, out, s, true, counts);
+    return check_launch(c, "render_fragments");
+}
+
 extern "C" int unimgs_deform(const unimgs_gaussians *rest, const unimgs_binding *b, const unimgs_vertex_field *f,
                              float *means_out, float *cov_out, void *stream) {
     if (!rest || !b || !f || !means_out || !cov_out) return UNIMGS_ERR_INVALID_ARGUMENT;

@@ -331,10 +331,14 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
                                                                      const TriRecord *__restrict__ trec, TexView tv,
                                                                      unsigned F, int W, int H, int tiles_x,
                                                                      BlendParams bp, float4 *__restrict__ out,
-                                                                     DevState *st) {
+                                                                     DevState *st, uint4 *__restrict__ frag_counts) {
     if (st->overflow) return;
     constexpr int NW = kBlendThreads / 32;  // warps per tile
-    unsigned long long w_gt = 0, w_gf = 0, w_tt = 0, w_tf = 0;  // COUNT only
+    // COUNT only: per lane (= per pixel) Gaussian / triangle entries tested and fragments
+    // blended, and the unified id of the last fragment blended
+    unsigned long long w_gt = 0, w_gf = 0, w_tt = 0, w_tf = 0;
+    unsigned last_id = 0xFFFFFFFFu;
+    __shared__ unsigned s_ids[COUNT ? NW : 1][32];  // COUNT only: packed entry k's id
     __shared__ WarpBuf s_buf[NW];
     __shared__ float4 s_stage[NW][32][3];  // this lane's record of the next chunk (cp.async)
     __shared__ TriAttr s_tri[NW][32];      // a packed triangle entry's q2..q5 (cp.async)
@@ -386,7 +390,10 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
     // Eq.1-2 blend of Gaussian fragment k (membership already decided bit-exactly):
     // alpha = min(alpha_max, o e^{-q/2}) = min(alpha_max, 2^(q kexp + log2 o))
     auto gblend = [&](float q, unsigned k) {
-        if (COUNT) w_gf++;
+        if (COUNT) {
+            w_gf++;
+            last_id = s_ids[COUNT ? warp : 0][k];
+        }
         const float4 ec = wb.col[k];
         const float al = fminf(bp.alpha_max, ex2_ftz(fmaf(q, kexp, ec.w)));
         if (MODE == MODE_WHOLE_PIXEL && s.open) {
@@ -441,6 +448,7 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
         const bool has_tri = __any_sync(0xffffffffu, rel && id < F);
         const unsigned cnt = __popc(bal);
         const unsigned slot = __popc(bal & lt);
+        if (COUNT && rel) s_ids[COUNT ? warp : 0][slot] = id;
         if (rel) {
             float *e = ef + 12 * (slot >> 1) + (slot & 1);
             if (id >= F) {
@@ -493,7 +501,10 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
                     const float w = h ? s.T * al[k] : 0.f;
                     s.C0 += w * ec[k].x; s.C1 += w * ec[k].y; s.C2 += w * ec[k].z;
                     s.T -= w;  // a fragment closes an open entity: T != Tlast
-                    if (COUNT && h) w_gf++;
+                    if (COUNT && h) {
+                        w_gf++;
+                        last_id = s_ids[COUNT ? warp : 0][2 * p + k];
+                    }
                 }
                 if (s.T < bp.t_eps) s.finish();
             }
@@ -531,15 +542,20 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
                     const float4 ec = wb.col[k];
                     const int X[3] = {__float_as_int(e[0]), __float_as_int(e[4]), __float_as_int(e[8])};
                     const int Y[3] = {__float_as_int(e[2]), __float_as_int(e[6]), __float_as_int(ec.x)};
-                    if (!s.done())
+                    if (!s.done()) {
+                        const unsigned long long f0 = w_tf;
                         tri_pixel<COUNT, MODE, M>(s, X, Y, __float_as_int(ec.y), ec.z, tat[k], x, y, tv, bp.t_eps,
                                                   w_tt, w_tf);
+                        if (COUNT && w_tf != f0) last_id = __float_as_uint(ec.w);
+                    }
                 }
             }
         }
         __syncwarp();
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");  // no copy may outlive the CTA's shared memory
+    if (COUNT && frag_counts && x < W && y < H)
+        frag_counts[(size_t)y * W + x] = make_uint4((unsigned)w_gf, (unsigned)w_tf, last_id, (unsigned)w_gt);
     if (COUNT) {
         unsigned long long v[4] = {w_gt, w_gf, w_tt, w_tf};
 #pragma unroll
@@ -559,40 +575,41 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
 
 template <int MODE, int M>
 static void launch_mode(const Buffers &b, const MeshInput &m, const CamParams &cam, const BlendParams &bp, float *out,
-                        cudaStream_t s, bool count_work) {
+                        cudaStream_t s, bool count_work, uint32_t *frag_counts) {
     const int tiles = cam.tiles_x * cam.tiles_y;
     TexView tv{reinterpret_cast<const uchar4 *>(m.tex), m.tw, m.th};
     if (count_work)
         k_blend<true, MODE, M><<<tiles, kBlendThreads, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
                                                                         (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
-                                                                        reinterpret_cast<float4 *>(out), b.st);
+                                                                        reinterpret_cast<float4 *>(out), b.st,
+                                                                        reinterpret_cast<uint4 *>(frag_counts));
     else
         k_blend<false, MODE, M><<<tiles, kBlendThreads, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
                                                                          (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
-                                                                         reinterpret_cast<float4 *>(out), b.st);
+                                                                         reinterpret_cast<float4 *>(out), b.st, nullptr);
 }
 
 template <int MODE>
 static void launch_m(int M, const Buffers &b, const MeshInput &m, const CamParams &cam, const BlendParams &bp,
-                     float *out, cudaStream_t s, bool count_work) {
+                     float *out, cudaStream_t s, bool count_work, uint32_t *fc) {
     switch (M) {
-        case 1: launch_mode<MODE, 1>(b, m, cam, bp, out, s, count_work); break;
-        case 2: launch_mode<MODE, 2>(b, m, cam, bp, out, s, count_work); break;
-        case 8: launch_mode<MODE, 8>(b, m, cam, bp, out, s, count_work); break;
-        case 16: launch_mode<MODE, 16>(b, m, cam, bp, out, s, count_work); break;
-        default: launch_mode<MODE, 4>(b, m, cam, bp, out, s, count_work); break;
+        case 1: launch_mode<MODE, 1>(b, m, cam, bp, out, s, count_work, fc); break;
+        case 2: launch_mode<MODE, 2>(b, m, cam, bp, out, s, count_work, fc); break;
+        case 8: launch_mode<MODE, 8>(b, m, cam, bp, out, s, count_work, fc); break;
+        case 16: launch_mode<MODE, 16>(b, m, cam, bp, out, s, count_work, fc); break;
+        default: launch_mode<MODE, 4>(b, m, cam, bp, out, s, count_work, fc); break;
     }
 }
 
 int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, const CamParams &cam,
-                 const BlendParams &bp, float *out, cudaStream_t s, bool count_work) {
+                 const BlendParams &bp, float *out, cudaStream_t s, bool count_work, uint32_t *fc) {
     (void)g;
     switch (bp.mode) {
-        case MODE_NAIVE: launch_m<MODE_NAIVE>(bp.msaa, b, m, cam, bp, out, s, count_work); break;
-        case MODE_MSAA_PIXEL: launch_m<MODE_MSAA_PIXEL>(bp.msaa, b, m, cam, bp, out, s, count_work); break;
-        case MODE_WHOLE_PIXEL: launch_m<MODE_WHOLE_PIXEL>(bp.msaa, b, m, cam, bp, out, s, count_work); break;
-        case MODE_PAPER_LITERAL: launch_m<MODE_PAPER_LITERAL>(bp.msaa, b, m, cam, bp, out, s, count_work); break;
-        default: launch_m<MODE_EXACT>(bp.msaa, b, m, cam, bp, out, s, count_work); break;
+        case MODE_NAIVE: launch_m<MODE_NAIVE>(bp.msaa, b, m, cam, bp, out, s, count_work, fc); break;
+        case MODE_MSAA_PIXEL: launch_m<MODE_MSAA_PIXEL>(bp.msaa, b, m, cam, bp, out, s, count_work, fc); break;
+        case MODE_WHOLE_PIXEL: launch_m<MODE_WHOLE_PIXEL>(bp.msaa, b, m, cam, bp, out, s, count_work, fc); break;
+        case MODE_PAPER_LITERAL: launch_m<MODE_PAPER_LITERAL>(bp.msaa, b, m, cam, bp, out, s, count_work, fc); break;
+        default: launch_m<MODE_EXACT>(bp.msaa, b, m, cam, bp, out, s, count_work, fc); break;
     }
     return 1;
 }

@@ -136,8 +136,12 @@ int64_t sort_lookback_tiles(int64_t max_pairs, int64_t max_prims);
 // at 64 so four fit beside nothing else, one leaves 3/4 of the SM to other streams)
 int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam, int sort_mode, int tri_depth,
                cudaStream_t s, int sm_count, int sort_per_sm);
+// count_work: the counting variant (DevState::work); frag_counts (counting variant only,
+// may be NULL): per pixel uint4 {Gaussian fragments blended, triangle fragments blended,
+// id of the last fragment blended (0xFFFFFFFF: none), Gaussian entries tested}
 int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, const CamParams &cam,
-                 const BlendParams &bp, float *out, cudaStream_t s, bool count_work = false);
+                 const BlendParams &bp, float *out, cudaStream_t s, bool count_work = false,
+                 uint32_t *frag_counts = nullptr);
 int launch_tile_stats(const Buffers &b, int tiles, cudaStream_t s);
 int launch_deform(const DeformInput &d, float *mu_out, float *cov_out, cudaStream_t s);
 // ray-cast binding (bind.cu): builds an LBVH in stream-ordered scratch; -1 if that allocation fails

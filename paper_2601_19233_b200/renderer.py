@@ -185,6 +185,17 @@ class Renderer:
         self._check(self.L.unimgs_render_counted(self._h, C.c_void_p(out.data_ptr()), w, _stream_handle(stream)))
         return out, dict(gauss_tests=w[0], gauss_frags=w[1], tri_tests=w[2], tri_frags=w[3])
 
+    def render_fragments(self, out: Optional[torch.Tensor] = None, stream=None):
+        """Render through the counting kernel (unimgs_render_fragments); returns (out, counts)
+        with counts [H, W, 4] int32: Gaussian fragments blended, triangle fragments blended,
+        id of the last fragment blended (-1 = none), Gaussian entries tested."""
+        if out is None:
+            out = torch.empty((self._cam.height, self._cam.width, 4), dtype=torch.float32, device="cuda")
+        counts = torch.empty((self._cam.height, self._cam.width, 4), dtype=torch.int32, device="cuda")
+        self._check(self.L.unimgs_render_fragments(self._h, C.c_void_p(out.data_ptr()), C.c_void_p(counts.data_ptr()),
+                                                   _stream_handle(stream)))
+        return out, counts
+
     def render_view(self, scene: DeviceScene, cam: SceneCamera, out=None, stream=None) -> torch.Tensor:
         self.preprocess(scene, cam, stream)
         self.bin(stream)

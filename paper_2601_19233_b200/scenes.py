@@ -554,6 +554,34 @@ def make_degenerate(seed=13, W=96, H=80):
     return Scene("degenerate", gall, mall, base.cameras, base.bg, base.bg_alpha), base
 
 
+def make_needles(seed=17, n=2000, W=256, H=256, kappa=(850.0, 1150.0)) -> Scene:
+    """Adversarial membership scene (P:300 / S:173 fragment membership; blend.cu's
+    per-warp culling): needle Gaussians whose projected conic condition number
+    straddles the culling-exactness threshold (~1000), i.e. cov2d eigenvalues
+    lambda_2 ~ 0.31 px^2 (dilation 0.3 dominated) and lambda_1 = kappa lambda_2 with
+    kappa ~ U(850, 1150): ~115 px long, ~3.5 px wide, random in-plane angle,
+    positions and opacities (so q_max varies), crossing 8x4 warp sub-tile edges
+    everywhere.  Identity camera, f = W."""
+    rng = np.random.default_rng(seed)
+    f = float(W)
+    cam = Camera(W, H, f, f, W / 2.0 + 0.137, H / 2.0 - 0.219, np.eye(3, dtype=np.float32), np.zeros(3, np.float32))
+    z = rng.uniform(2.0, 6.0, n)
+    u = rng.uniform(-20.0, W + 20.0, n)
+    v = rng.uniform(-20.0, H + 20.0, n)
+    means = np.stack([(u - cam.cx) / f * z, (v - cam.cy) / f * z, z], -1)
+    lam2 = 0.31
+    lam1 = rng.uniform(kappa[0], kappa[1], n) * lam2
+    s1 = z / f * np.sqrt(lam1 - 0.3)
+    s2 = z / f * 0.1
+    scales = np.stack([s1, s2, np.full(n, 1e-4)], -1)
+    th = rng.uniform(0.0, np.pi, n)  # rotation about the view axis
+    quats = np.stack([np.cos(th / 2), np.zeros(n), np.zeros(n), np.sin(th / 2)], -1)
+    opac = rng.uniform(0.05, 1.0, n)
+    sh = ((rng.uniform(0.1, 0.9, (n, 1, 3)) - 0.5) / SH_C0)
+    g = _pack_gaussians(means, quats, scales, opac, sh, 0)
+    return Scene("needles", g, empty_mesh(), [cam], bg=np.array([0.02, 0.03, 0.05], np.float32))
+
+
 # ----------------------------------------------------------------------------
 # pin constructions for the shading steps (bilinear texture, SH view direction,
 # 1.3x FoV Jacobian clamp).  Geometry and inputs only; the expected values are
