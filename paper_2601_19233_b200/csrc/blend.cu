@@ -136,30 +136,38 @@ __device__ __forceinline__ void tri_colour(const TriAttr &r, int kind, const lon
     }
 }
 
-// Exact per-warp culling (never drops a fragment).  Warp w owns the 8x4
-// sub-tile (w & 1, w >> 1) of the 16x16 tile; an entry is skipped by the warp
-// only when no pixel of its sub-tile can hold the fragment:
-//   triangle: its snapped integer bbox misses the sub-tile's 1/256-px extent;
-//   Gaussian: the sub-tile's pixel centres lie outside the bbox of the exact
+// Exact per-warp culling (never drops a fragment of a live pixel).  Warp w owns
+// the 8x4 sub-tile (w & 1, w >> 1) of the 16x16 tile; the culling rectangle is
+// the bounding box of the sub-tile's pixels that have not terminated yet (it
+// shrinks as pixels finish: a finished pixel consumes no entry), and an entry
+// is skipped by the warp only when no pixel of that box can hold the fragment:
+//   triangle: its snapped integer bbox misses the box's 1/256-px extent;
+//   Gaussian: the box's pixel centres lie outside the bbox of the exact
 //   ellipse {d : Q(d) <= q_max (1 + 0.02)} of the fp32 conic Q, padded by
 //   1% + 0.01 px (half-extents computed once per Gaussian in B1).  Only for
 //   cond(Q) <= ~1000, where the fp32 evaluation of q (10 roundings,
 //   cancellation factor <= 2(cond + 1)) errs by < 1.3e-3 q, so a pixel outside
 //   that ellipse cannot satisfy the N6 test q <= q_max.  Other conics
 //   (needles, NaN) are never skipped.
-__device__ __forceinline__ bool gauss_touches(const float4 &a, const float4 &b, const float4 &c, float rx0, float ry0,
-                                              float ry1) {
+// The box: pixel-centre extents [cx0, cx1] x [cy0, cy1] (px) and the covered
+// 1/256-px extents [X0, X1] x [Y0, Y1] of the live pixels.
+struct LiveBox {
+    float cx0, cx1, cy0, cy1;
+    int X0, X1, Y0, Y1;
+};
+
+__device__ __forceinline__ bool gauss_touches(const float4 &a, const float4 &b, const float4 &c, const LiveBox &lb) {
     const float ex = c.w, ey = b.w;  // precomputed in B1; -1 = never cull
     if (!(ex >= 0.f)) return true;
-    return a.x + ex >= rx0 && a.x - ex <= rx0 + 7.f && a.y + ey >= ry0 && a.y - ey <= ry1;
+    return a.x + ex >= lb.cx0 && a.x - ex <= lb.cx1 && a.y + ey >= lb.cy0 && a.y - ey <= lb.cy1;
 }
 
-__device__ __forceinline__ bool tri_touches(const float4 &a, const float4 &b, int Rx0, int Ry0, int Ry1) {
+__device__ __forceinline__ bool tri_touches(const float4 &a, const float4 &b, const LiveBox &lb) {
     const int X0 = __float_as_int(a.x), Y0 = __float_as_int(a.y), X1 = __float_as_int(a.z), Y1 = __float_as_int(a.w);
     const int X2 = __float_as_int(b.x), Y2 = __float_as_int(b.y);
     const int mnx = min(X0, min(X1, X2)), mxx = max(X0, max(X1, X2));
     const int mny = min(Y0, min(Y1, Y2)), mxy = max(Y0, max(Y1, Y2));
-    return mxx >= Rx0 && mnx <= Rx0 + 256 * 8 - 1 && mxy >= Ry0 && mny <= Ry1;
+    return mxx >= lb.X0 && mnx <= lb.X1 && mxy >= lb.Y0 && mny <= lb.Y1;
 }
 
 __device__ __forceinline__ float lg2_ftz(float x) {  // x = o >= 1/255: never subnormal
@@ -349,8 +357,6 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
     const int sx0 = tx * kTile + (warp & 1) * 8, sy0 = ty * kTile + (warp >> 1) * 4;
     const int x = sx0 + (lane & 7), y = sy0 + (lane >> 3);
     const float px = (float)x + 0.5f;
-    const float rx0 = (float)sx0 + 0.5f, ry0 = (float)sy0 + 0.5f, ry1 = ry0 + 3.f;
-    const int Rx0 = 256 * sx0, Ry0 = 256 * sy0, Ry1 = 256 * (sy0 + 4) - 1;
     const uint2 rg = ranges[tile];
     const unsigned lt = (1u << lane) - 1u;
     WarpBuf &wb = s_buf[warp];
@@ -427,7 +433,23 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
     };
 
     for (unsigned base = rg.x; base < rg.y; base += 32) {
-        if (__all_sync(0xffffffffu, s.done())) break;
+        // the live pixels' bounding box (lane = 8 row + column)
+        const unsigned live = __ballot_sync(0xffffffffu, !s.done());
+        if (!live) break;
+        LiveBox lb;
+        {
+            const unsigned cols = (live | (live >> 8) | (live >> 16) | (live >> 24)) & 0xFFu;
+            const int c0 = __ffs(cols) - 1, c1 = 31 - __clz(cols);
+            const int r0 = (__ffs(live) - 1) >> 3, r1 = (31 - __clz(live)) >> 3;
+            lb.cx0 = (float)(sx0 + c0) + 0.5f;
+            lb.cx1 = (float)(sx0 + c1) + 0.5f;
+            lb.cy0 = (float)(sy0 + r0) + 0.5f;
+            lb.cy1 = (float)(sy0 + r1) + 0.5f;
+            lb.X0 = 256 * (sx0 + c0);
+            lb.X1 = 256 * (sx0 + c1 + 1) - 1;
+            lb.Y0 = 256 * (sy0 + r0);
+            lb.Y1 = 256 * (sy0 + r1 + 1) - 1;
+        }
         const unsigned id = id0;
         id0 = id1;
         id1 = base + 64 + lane < rg.y ? __ldg(vals + base + 64 + lane) : 0xFFFFFFFFu;
@@ -439,9 +461,9 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
             b = stg[1];
             if (id >= F) {
                 c = stg[2];
-                rel = gauss_touches(a, b, c, rx0, ry0, ry1);
+                rel = gauss_touches(a, b, c, lb);
             } else {
-                rel = tri_touches(a, b, Rx0, Ry0, Ry1);
+                rel = tri_touches(a, b, lb);
             }
         }
         const unsigned bal = __ballot_sync(0xffffffffu, rel);
