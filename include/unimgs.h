@@ -337,6 +337,13 @@ UNIMGS_API int unimgs_set_host_lanes(unimgs_ctx *c, int32_t lanes);
  * clears): the frames of that batch in out_host are then not all valid. */
 UNIMGS_API int unimgs_host_wait(unimgs_ctx *c);
 
+/* Checked build only (libunimgs_checked.so, -DUNIMGS_CHECKED: device bounds
+ * checks that trap on a violated index, and a 4 KiB guard band after every
+ * context scratch buffer): synchronises the device and writes to *bad_bytes
+ * (host) the number of guard bytes overwritten, over this context and its host
+ * lanes.  The production library returns UNIMGS_ERR_UNSUPPORTED. */
+UNIMGS_API int unimgs_debug_check_guards(unimgs_ctx *c, int64_t *bad_bytes);
+
 /* Number of kernel launches enqueued by this context since creation. */
 UNIMGS_API int64_t unimgs_launch_count(const unimgs_ctx *c);
 

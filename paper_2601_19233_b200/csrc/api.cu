@@ -4,9 +4,11 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/unimgs.h"
@@ -53,7 +55,30 @@ struct unimgs_ctx {
     // another lane's compute-bound blend (DESIGN.md §5 history)
     cudaStream_t bin_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_binned = nullptr;
+    // checked build only: every scratch buffer is followed by a guard band of kGuardBytes
+    // filled with kGuardByte (unimgs_debug_check_guards counts the bytes overwritten)
+    std::vector<std::pair<void *, size_t>> guards;
 };
+
+[[maybe_unused]] static constexpr size_t kGuardBytes = 4096;
+[[maybe_unused]] static constexpr unsigned char kGuardByte = 0x5A;
+
+// cudaMalloc of a context scratch buffer (+ the guard band in the checked build)
+static cudaError_t dev_alloc(unimgs_ctx *c, void **p, size_t bytes) {
+#ifdef UNIMGS_CHECKED
+    cudaError_t e = cudaMalloc(p, bytes + kGuardBytes);
+    if (e != cudaSuccess) return e;
+    c->guards.push_back({*p, bytes});
+    return cudaMemset(static_cast<char *>(*p) + bytes, kGuardByte, kGuardBytes);
+#else
+    (void)c;
+    return cudaMalloc(p, bytes);
+#endif
+}
+template <typename T>
+static cudaError_t dev_alloc(unimgs_ctx *c, T **p, size_t bytes) {
+    return dev_alloc(c, reinterpret_cast<void **>(p), bytes);
+}
 
 extern "C" void unimgs_destroy(unimgs_ctx *c);
 
@@ -161,6 +186,7 @@ static void free_buffers(unimgs_ctx *c) {
     for (void *p : ptrs)
         if (p) cudaFree(p);
     memset(&b, 0, sizeof b);
+    c->guards.clear();
     c->reserved = false;
 }
 
@@ -177,26 +203,39 @@ extern "C" int unimgs_reserve2(unimgs_ctx *c, int64_t max_gaussians, int64_t max
     const int64_t P = max_gaussians + max_triangles + 1;
     const int64_t tiles = (int64_t)((max_w + 15) / 16) * ((max_h + 15) / 16);
     const int64_t lb_tiles = sort_lookback_tiles(max_pairs, P);
-    CUDA_TRY(c, cudaMalloc(&b.rect, sizeof(uint2) * P));
-    CUDA_TRY(c, cudaMalloc(&b.touched, sizeof(uint32_t) * P));
-    CUDA_TRY(c, cudaMalloc(&b.dkey, sizeof(uint32_t) * P));
-    CUDA_TRY(c, cudaMalloc(&b.grec, sizeof(GaussRecord) * (max_gaussians + 1)));
-    CUDA_TRY(c, cudaMalloc(&b.trec, sizeof(TriRecord) * (max_triangles + 1)));
+    const int64_t n_rstart = max_pairs / 1024 + 2;
+    CUDA_TRY(c, dev_alloc(c, &b.rect, sizeof(uint2) * P));
+    CUDA_TRY(c, dev_alloc(c, &b.touched, sizeof(uint32_t) * P));
+    CUDA_TRY(c, dev_alloc(c, &b.dkey, sizeof(uint32_t) * P));
+    CUDA_TRY(c, dev_alloc(c, &b.grec, sizeof(GaussRecord) * (max_gaussians + 1)));
+    CUDA_TRY(c, dev_alloc(c, &b.trec, sizeof(TriRecord) * (max_triangles + 1)));
     for (int i = 0; i < 2; i++) {
-        CUDA_TRY(c, cudaMalloc(&b.pk[i], sizeof(uint32_t) * P));
-        CUDA_TRY(c, cudaMalloc(&b.pv[i], sizeof(uint32_t) * P));
-        CUDA_TRY(c, cudaMalloc(&b.tk[i], sizeof(uint64_t) * max_pairs));
-        CUDA_TRY(c, cudaMalloc(&b.tv[i], sizeof(uint32_t) * max_pairs));
+        CUDA_TRY(c, dev_alloc(c, &b.pk[i], sizeof(uint32_t) * P));
+        CUDA_TRY(c, dev_alloc(c, &b.pv[i], sizeof(uint32_t) * P));
+        CUDA_TRY(c, dev_alloc(c, &b.tk[i], sizeof(uint64_t) * max_pairs));
+        CUDA_TRY(c, dev_alloc(c, &b.tv[i], sizeof(uint32_t) * max_pairs));
     }
-    CUDA_TRY(c, cudaMalloc(&b.ranges, sizeof(uint2) * tiles));
-    CUDA_TRY(c, cudaMalloc(&b.order, sizeof(uint32_t) * tiles));
-    CUDA_TRY(c, cudaMalloc(&b.bcnt, sizeof(uint32_t) * (size_t)(max_gaussians / 256 + max_triangles / 256 + 4)));
-    CUDA_TRY(c, cudaMalloc(&b.dcnt, sizeof(uint32_t) * (size_t)(P / 2048 + 4)));
-    CUDA_TRY(c, cudaMalloc(&b.rstart, sizeof(uint32_t) * (size_t)(max_pairs / 1024 + 2)));
-    CUDA_TRY(c, cudaMalloc(&b.lookback, sizeof(unsigned long long) * 256 * lb_tiles));
-    CUDA_TRY(c, cudaMalloc(&b.st, sizeof(DevState)));
+    CUDA_TRY(c, dev_alloc(c, &b.ranges, sizeof(uint2) * tiles));
+    CUDA_TRY(c, dev_alloc(c, &b.order, sizeof(uint32_t) * tiles));
+    CUDA_TRY(c, dev_alloc(c, &b.bcnt, sizeof(uint32_t) * (size_t)(max_gaussians / 256 + max_triangles / 256 + 4)));
+    CUDA_TRY(c, dev_alloc(c, &b.dcnt, sizeof(uint32_t) * (size_t)(P / 2048 + 4)));
+    CUDA_TRY(c, dev_alloc(c, &b.rstart, sizeof(uint32_t) * (size_t)n_rstart));
+    CUDA_TRY(c, dev_alloc(c, &b.lookback, sizeof(unsigned long long) * 256 * lb_tiles));
+    CUDA_TRY(c, dev_alloc(c, &b.st, sizeof(DevState)));
     CUDA_TRY(c, cudaMemset(b.lookback, 0, sizeof(unsigned long long) * 256 * lb_tiles));
     CUDA_TRY(c, cudaMemset(b.st, 0, sizeof(DevState)));
+    {
+        unsigned caps[4] = {(unsigned)P, (unsigned)max_pairs, (unsigned)tiles, (unsigned)n_rstart};
+#ifdef UNIMGS_CHECKED
+        // fault injection for the checked build's self-test (tests/test_gpu_checked.py):
+        // a 1-tile capacity makes every tile index >= 1 trip UNIMGS_CHECK; a cleared guard
+        // byte must be reported by unimgs_debug_check_guards
+        if (getenv("UNIMGS_FAULT_TILES")) caps[2] = 1;
+        if (getenv("UNIMGS_FAULT_GUARD") && !c->guards.empty())
+            CUDA_TRY(c, cudaMemset(static_cast<char *>(c->guards[0].first) + c->guards[0].second, 0, 1));
+#endif
+        CUDA_TRY(c, cudaMemcpy(&b.st->cap_prims, caps, sizeof caps, cudaMemcpyHostToDevice));
+    }
     CUDA_TRY(c, cudaMemset(b.ranges, 0, sizeof(uint2) * tiles));
     CUDA_TRY(c, cudaDeviceSynchronize());
     b.max_prims = P - 1;
@@ -669,6 +708,26 @@ extern "C" int unimgs_render_host(unimgs_ctx *c, const unimgs_gaussians *gh, con
     int rc = unimgs_render_host_async(c, gh, mh, cams, n_views, out_host, stream);
     if (rc) return rc;
     return unimgs_host_wait(c);
+}
+
+extern "C" int unimgs_debug_check_guards(unimgs_ctx *c, int64_t *bad_bytes) {
+    if (!c || !bad_bytes) return UNIMGS_ERR_INVALID_ARGUMENT;
+    *bad_bytes = 0;
+#ifdef UNIMGS_CHECKED
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    std::vector<unsigned char> h(kGuardBytes);
+    for (int l = 0; l < c->lanes; l++) {
+        unimgs_ctx *x = l ? c->child[l] : c;
+        for (const auto &g : x->guards) {
+            CUDA_TRY(c, cudaMemcpy(h.data(), static_cast<char *>(g.first) + g.second, kGuardBytes,
+                                   cudaMemcpyDeviceToHost));
+            for (unsigned char v : h) *bad_bytes += v != kGuardByte;
+        }
+    }
+    return UNIMGS_OK;
+#else
+    return fail(c, UNIMGS_ERR_UNSUPPORTED, "guard bands exist only in the checked build (libunimgs_checked.so)");
+#endif
 }
 
 extern "C" int64_t unimgs_launch_count(const unimgs_ctx *c) {

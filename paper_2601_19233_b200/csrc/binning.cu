@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(1024) k_scan_counts(uint32_t *cnt, int64_t n, 
 // One CTA per 256 primitives, in the block order of B2 (triangles) then B1 (Gaussians).
 __global__ void __launch_bounds__(256) k_compact(int64_t F, int64_t N, int nbt, const uint32_t *__restrict__ touched,
                                                  const uint32_t *__restrict__ dkey, const uint32_t *__restrict__ boff,
-                                                 uint32_t *ok, uint32_t *ov) {
+                                                 uint32_t *ok, uint32_t *ov, const DevState *st) {
     __shared__ unsigned s_c[8];
     const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int blk = blockIdx.x;
@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(256) k_compact(int64_t F, int64_t N, int nbt, 
     if (v) {
         unsigned pos = boff[blk] + __popc(bal & ((1u << lane) - 1u));
         for (unsigned w = 0; w < wid; w++) pos += s_c[w];
+        UNIMGS_CHECK(pos < st->cap_prims);
         ok[pos] = dkey[p];
         ov[pos] = (uint32_t)p;
     }
@@ -237,6 +238,7 @@ __global__ void __launch_bounds__(kScanThreads) k_dup_count(const uint32_t *__re
 #pragma unroll
     for (int i = 0; i < kScanItems; i++) {  // in-chunk exclusive prefix of each sorted position
         const int64_t j = base + e0 + 32 * i;
+        UNIMGS_CHECK(j >= n || j < st->cap_prims);
         if (j < n) prel[j] = ex[i];
     }
     if (threadIdx.x == kScanThreads - 1) dcnt[blockIdx.x] = sat_add(ex[kScanItems - 1], v[kScanItems - 1]);
@@ -320,8 +322,10 @@ __global__ void k_range_starts(const uint32_t *__restrict__ dcnt, const uint32_t
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const unsigned off = dcnt[i / kScanTile] + prel[i];
         const unsigned nxt = i + 1 < n ? dcnt[(i + 1) / kScanTile] + prel[i + 1] : K;
-        for (unsigned r = (off + slots - 1) / slots; (unsigned long long)r * slots < nxt && r * slots < K; r++)
+        for (unsigned r = (off + slots - 1) / slots; (unsigned long long)r * slots < nxt && r * slots < K; r++) {
+            UNIMGS_CHECK(r < st->cap_rstart);
             rstart[r] = i;
+        }
     }
 }
 
@@ -362,6 +366,7 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
         const unsigned p0 = rstart[r];
         const unsigned p1 = r + 1 < nranges ? rstart[r + 1] : n - 1;  // holds slot E (or E - 1)
         const int m = (int)(p1 - p0) + 1;
+        UNIMGS_CHECK(m >= 1 && m + 1 <= MP && p1 < n);
         __syncthreads();  // previous range's staging consumed
         for (int j = threadIdx.x; j < m; j += kScanThreads) {
             const unsigned i = p0 + j;
@@ -389,6 +394,7 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
                 const unsigned qq = local / w;
                 const unsigned tx = x0 + (local - qq * w), ty = y0 + qq;
                 const unsigned t = ty * (unsigned)tiles_x + tx;
+                UNIMGS_CHECK(e < m && t < st->cap_tiles && S + (unsigned)k < st->cap_pairs);
                 const uint32_t pid = s_id[e];
                 if (FULL) {
                     uint32_t d = s_dk[FULL ? e : 0];
@@ -556,6 +562,7 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
             if (wbase + 32u * i < n) {
                 const unsigned d = (unsigned)((key[i] >> shift) & mask);
                 const unsigned pos = s_doff[d] + wh[d] + rank[i];
+                UNIMGS_CHECK(pos < (unsigned)TILE_);
                 s_k[pos] = key[i];
                 s_v[pos] = val[i];
             }
@@ -592,6 +599,7 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
             const KT kk = s_k[k];
             const unsigned d = (unsigned)((kk >> shift) & mask);
             const unsigned o = (unsigned)(s_glob[d] + (int)k);
+            UNIMGS_CHECK(o < n);
             kout[o] = kk;
             vout[o] = s_v[k];
         }
@@ -623,6 +631,7 @@ __global__ void __launch_bounds__(256) k_ranges16(const uint16_t *__restrict__ k
         for (int j = 0; j < 8; j++) {
             if (i0 + j >= n) break;
             const unsigned cur = k[j];
+            UNIMGS_CHECK(cur < st->cap_tiles);
             const unsigned pv = j ? (unsigned)k[j - 1] : prev;
             const unsigned nx = (j < 7 && i0 + j + 1 < n) ? (unsigned)k[j + 1] : (i0 + j + 1 < n ? next : 0xFFFFFFFFu);
             if (cur != pv) ranges[cur].x = i0 + j;
@@ -637,6 +646,7 @@ __global__ void k_ranges64(const unsigned long long *__restrict__ keys, const un
     const unsigned n = *n_ptr;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const unsigned tl = (unsigned)(keys[i] >> 32);
+        UNIMGS_CHECK(tl < st->cap_tiles);
         const unsigned prev = i > 0 ? (unsigned)(keys[i - 1] >> 32) : 0xFFFFFFFFu;
         const unsigned next = i + 1 < n ? (unsigned)(keys[i + 1] >> 32) : 0xFFFFFFFFu;
         if (tl != prev) ranges[tl].x = i;
@@ -751,7 +761,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
     const int nbt = (int)((F + 255) / 256), nbg = (int)((N + 255) / 256);
     if (P > 0) {
         k_scan_counts<<<1, 1024, 0, s>>>(b.bcnt, nbt + nbg, 0, 0, b.st);
-        k_compact<<<nbt + nbg, 256, 0, s>>>(F, N, nbt, b.touched, b.dkey, b.bcnt, b.pk[0], b.pv[0]);
+        k_compact<<<nbt + nbg, 256, 0, s>>>(F, N, nbt, b.touched, b.dkey, b.bcnt, b.pk[0], b.pv[0], b.st);
         launches += 2;
     }
     int slot = SLOT_PASS0;

@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
     const int x = sx0 + (lane & 7), y = sy0 + (lane >> 3);
     const float px = (float)x + 0.5f;
     const uint2 rg = ranges[tile];
+    UNIMGS_CHECK((unsigned)tile < st->cap_tiles && rg.x <= rg.y && rg.y <= st->K);
     const unsigned lt = (1u << lane) - 1u;
     WarpBuf &wb = s_buf[warp];
     float *ef = &wb.e[0][0].x;
@@ -470,6 +471,7 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
         const bool has_tri = __any_sync(0xffffffffu, rel && id < F);
         const unsigned cnt = __popc(bal);
         const unsigned slot = __popc(bal & lt);
+        UNIMGS_CHECK(!rel || (slot < 32u && id < st->cap_prims));
         if (COUNT && rel) s_ids[COUNT ? warp : 0][slot] = id;
         if (rel) {
             float *e = ef + 12 * (slot >> 1) + (slot & 1);

@@ -3,8 +3,27 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace unimgs {
+
+// Bounds checks of the checked build (-DUNIMGS_CHECKED, paper_2601_19233_b200/
+// libunimgs_checked.so): a violated index trap-kills the kernel with a message, so
+// the launch fails loudly.  Compiled out of the production library.
+#ifdef UNIMGS_CHECKED
+#define UNIMGS_CHECK(c)                                                                                    \
+    do {                                                                                                   \
+        if (!(c)) {                                                                                        \
+            printf("UNIMGS_CHECK failed: %s (%s:%d, block %d thread %d)\n", #c, __FILE__, __LINE__,        \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                     \
+            __trap();                                                                                      \
+        }                                                                                                  \
+    } while (0)
+#else
+#define UNIMGS_CHECK(c) \
+    do {                \
+    } while (0)
+#endif
 
 constexpr int kTile = 16;
 constexpr int kBlendThreads = 256;
@@ -12,11 +31,14 @@ constexpr int kMaxPasses = 8;
 
 // Per-frame device counters.  frame_epoch survives across frames (it tags
 // decoupled-look-back entries so the look-back buffers never need clearing) and so
-// does overflow_sticky; everything after them is zeroed by k_begin_frame.
+// do overflow_sticky and the capacities; everything from n_vis on is zeroed by
+// k_begin_frame.
 struct DevState {
     unsigned int frame_epoch;
     unsigned int overflow_sticky;  // set by any frame that overflowed; cleared only by unimgs_host_wait
-    unsigned int n_vis;         // visible primitives (compacted)
+    // capacities written by unimgs_reserve (read by the UNIMGS_CHECKED bounds checks)
+    unsigned int cap_prims, cap_pairs, cap_tiles, cap_rstart;
+    unsigned int n_vis;         // visible primitives (compacted) -- first field k_begin_frame zeroes
     unsigned int K;             // pairs written (0 on overflow)
     unsigned long long needed;  // pairs required (saturating at 2^32-1)
     unsigned int overflow;

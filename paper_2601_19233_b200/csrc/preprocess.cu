@@ -5,6 +5,8 @@
 // DESIGN.md "normative fp32 arithmetic" N1-N7 with explicit round-to-nearest
 // intrinsics (no FMA contraction), so the keys are bit-identical to the
 // independent CPU oracle.  Colour (SH) is ordinary fp32.
+#include <cstddef>
+
 #include "internal.cuh"
 
 #ifndef UNIMGS_SH_PREFETCH
@@ -31,9 +33,9 @@ __device__ __forceinline__ void view_point(const CamParams &c, float x, float y,
 
 __global__ void k_begin_frame(DevState *st) {
     unsigned int *w = reinterpret_cast<unsigned int *>(st);
-    const int n = sizeof(DevState) / 4;
+    const int n = sizeof(DevState) / 4, first = offsetof(DevState, n_vis) / 4;
     if (threadIdx.x == 0) st->frame_epoch += 1;
-    for (int i = 2 + threadIdx.x; i < n; i += blockDim.x) w[i] = 0;
+    for (int i = first + threadIdx.x; i < n; i += blockDim.x) w[i] = 0;
 }
 
 int launch_begin_frame(DevState *st, cudaStream_t s) {
@@ -244,6 +246,7 @@ __global__ void __launch_bounds__(256, UNIMGS_PRE_MINB) k_preprocess_gaussians(G
             b.dkey[p] = __float_as_uint(pv[2]);
             vis = true;
         } while (0);
+        UNIMGS_CHECK(p < b.st->cap_prims);
         b.touched[p] = touched;
         if (!vis) b.dkey[p] = 0xFFFFFFFFu;
     }
@@ -343,6 +346,7 @@ __global__ void __launch_bounds__(256) k_setup_triangles(MeshInput m, CamParams 
             b.dkey[f] = __float_as_uint(depth);
             vis = true;
         } while (0);
+        UNIMGS_CHECK(f < b.st->cap_prims);
         b.touched[f] = touched;
         if (!vis) b.dkey[f] = 0xFFFFFFFFu;
     }

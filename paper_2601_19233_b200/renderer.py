@@ -275,6 +275,12 @@ class Renderer:
                     rect=unpacked.astype(np.int32), touched=touched[:P].cpu().numpy().view(np.uint32),
                     dkey=dkeys[:P].cpu().numpy().view(np.uint32))
 
+    def check_guards(self) -> int:
+        """Checked build only: guard-band bytes overwritten (unimgs_debug_check_guards)."""
+        bad = C.c_int64()
+        self._check(self.L.unimgs_debug_check_guards(self._h, C.byref(bad)))
+        return int(bad.value)
+
     def launch_count(self) -> int:
         return int(self.L.unimgs_launch_count(self._h))
 
