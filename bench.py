@@ -38,7 +38,7 @@ WORKLOAD = ("multiview: mip360-like 3M Gaussians (SH3) + 200k-triangle textured 
 OPS_GAUSS_TEST = 11      # dx, dy, 4 mul, 2 fma, compare
 OPS_GAUSS_FRAG = 12      # -q/2, exp, *o, min, T*a, 3 fma colour, T update (+ entity close test)
 OPS_TRI_TEST = 33        # 3 int64 edge functions at the centre + 12 sample offsets + 12 compares
-OPS_TRI_FRAG = 60        # fp64 perspective barycentrics, bilinear texture, entity update
+OPS_TRI_FRAG = 60        # perspective barycentrics, bilinear texture, entity update
 
 
 def parse():
@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--prio", type=int, default=1, help="1: preprocess+bin on high-priority streams (0: one stream per context)")
     ap.add_argument("--streams", type=int, default=4,
                     help="renderer contexts on separate CUDA streams; consecutive views overlap")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config single-view numbers (SURVEY §8(d) Reporting; rank 0, N = 1)")
     return ap.parse_args()
 
 
@@ -165,6 +167,13 @@ def run_reference(a, rank, world):
 # ----------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------
+def alg_bytes_survey(N, F, V, N_vis, F_vis, P, K, W, H):
+    """SURVEY §8(d)'s B_alg: every input byte once (N x 236 B at SH degree 3), records,
+    pairs written + sorted + read for ranges + read with their record, output once."""
+    return (N * 236 + V * 20 + F * 16 + N_vis * 48 + F_vis * 80 + P * 12 + K * (12 + 24 + 8 + 4 + 48)
+            + W * H * 16)
+
+
 def alg_bytes(N, F, V, N_vis, F_vis, P, K, W, H, sh_k=16):
     """Algorithmic HBM bytes of one frame: inputs once (SH of visible
     Gaussians only), records written once, pairs written once + sorted once + read for
@@ -173,11 +182,92 @@ def alg_bytes(N, F, V, N_vis, F_vis, P, K, W, H, sh_k=16):
             + K * (12 + 24 + 8 + 4 + 48) + W * H * 16)
 
 
+def world_info(world, gather, p2p):
+    """Ranks and the communicator the line was measured with (the driver checks them)."""
+    import torch
+    info = {"size": world, "rank_of_line": 0, "backend": None, "nccl_version": None,
+            "gather": "none" if not gather else ("fused P2P stores (CUDA IPC), device-side step flags" if p2p
+                                                 else "NCCL grouped send/recv to rank 0 on a comm stream"),
+            "devices": torch.cuda.device_count(), "device_name": torch.cuda.get_device_name(0)}
+    if world > 1:
+        import torch.distributed as dist
+        info["backend"] = dist.get_backend()
+        try:
+            info["nccl_version"] = ".".join(str(x) for x in torch.cuda.nccl.version())
+        except Exception:
+            pass
+    return info
+
+
+def graph_frame_times(sc, frames=200, warm=20):
+    """One context on one stream, the scene resident: `warm` eager frames, then `frames`
+    CUDA-graph replays of preprocess -> bin -> render, each bracketed by CUDA events."""
+    import numpy as np
+    import torch
+    from paper_2601_19233_b200 import renderer as R
+    cam = sc.cameras[0]
+    r = R.renderer_for(sc, max_pairs=24 << 20)
+    ds = R.to_device(sc)
+    out = torch.empty((cam.height, cam.width, 4), device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(warm):
+            r.render_view(ds, cam, out=out, stream=s)
+    torch.cuda.synchronize()
+    st = r.stats()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        r.render_view(ds, cam, out=out, stream=s)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(frames)]
+    with torch.cuda.stream(s):
+        for e0, e1 in ev:
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+    torch.cuda.synchronize()
+    ms = np.array([x.elapsed_time(y) for x, y in ev])
+    del g, r
+    return ms, st
+
+
+def config_numbers(cores):
+    """SURVEY §8(d) Reporting, per BASELINE.json config (one view each; the multiview batch is
+    the headline line): device-timed median / p95 frame time (CUDA-graph replay, 20 + 200
+    frames), the Fig.5a mirror (SPEC S:598 soft bound 2.0x): frame time with the
+    meshes / with the meshes removed, and the CPU oracle's seconds for the same frame
+    (single-threaded for tiny and nerf, all host cores for mip360 and stress)."""
+    import dataclasses
+    import numpy as np
+    from paper_2601_19233_b200 import scenes
+    res = {}
+    for name in ("tiny", "nerf", "mip360", "stress"):
+        sc = scenes.make_scene(name)
+        ms, st = graph_frame_times(sc)
+        med, p95 = float(np.median(ms)), float(np.percentile(ms, 95))
+        ent = {"median_ms": med, "p95_ms": p95, "fps_median": 1000.0 / med, "fps_p95": 1000.0 / p95,
+               "pairs": st["num_pairs"], "visible_gaussians": st["visible_gaussians"],
+               "visible_triangles": st["visible_triangles"]}
+        if name in ("mip360", "stress"):
+            bare = dataclasses.replace(sc, mesh=scenes.empty_mesh())
+            ms0, _ = graph_frame_times(bare)
+            ent["no_mesh_median_ms"] = float(np.median(ms0))
+            ent["mesh_over_no_mesh"] = med / float(np.median(ms0))
+        th = 1 if name in ("tiny", "nerf") else cores
+        t = oracle_frames(sc, sc.cameras[:1], th)[0]
+        ent["oracle_s"] = t
+        ent["oracle_threads"] = th
+        ent["gpu_over_oracle"] = t * 1000.0 / med
+        res[name] = ent
+    return res
+
+
 def run_ours(a, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2601_19233_b200 import renderer as R, scenes
-    from paper_2601_19233_b200.dist import P2PFrameGather, gather_frames, views_for_rank
+    from paper_2601_19233_b200.dist import P2PFrameGather, gather_frames, run_gather_pipeline, views_for_rank
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -198,6 +288,7 @@ def run_ours(a, rank, world, local_rank):
     # (torch maps a priority beyond the device's range to its highest priority)
     pstreams = [torch.cuda.Stream(device=dev, priority=-100) for _ in range(nS)] if a.prio else streams
     ds = R.to_device(sc, dev)
+    scene_gb = ds.nbytes() / 1e9
     V = a.views
 
     def views_of(step):
@@ -212,13 +303,15 @@ def run_ours(a, rank, world, local_rank):
     comm = torch.cuda.Stream(device=dev) if gather and p2p is None else None
     s = torch.cuda.current_stream()
 
-    def step_fn(step, ev_pairs=None):
+    def render_step(step, views, bi, ev_pairs=None):
         # view j of the step renders with context j % nS on stream j % nS: the
         # compute-bound blend of one view overlaps the binning of the next
-        buf = p2p.frames(step) if p2p is not None else frames[step & 1]
+        buf = p2p.frames(step) if p2p is not None else frames[bi]
         for st_ in streams:
-            st_.wait_stream(s)
-        for j, vi in enumerate(views_of(step)):
+            st_.wait_stream(s)  # (s carries the waits on the gather handles of step - 2)
+        if p2p is not None:
+            p2p.before_step(step, streams)  # rank 0 has released step - 2's slot (device-side)
+        for j, vi in enumerate(views):
             rr, ss_, ps_ = rs[j % nS], streams[j % nS], pstreams[j % nS]
             if ps_ is not ss_:
                 ps_.wait_stream(ss_)  # the context's previous blend has released its buffers
@@ -237,14 +330,14 @@ def run_ours(a, rank, world, local_rank):
         # No join at the end of a step: the next step's views queue behind this one's on
         # each context's streams (steps pipeline like the iterations of a serving loop);
         # the timed region joins all streams once, before its end event.
+
+    def post_step(step, bi):
         if not gather:
             return []
-        if p2p is not None:  # frames already stored in rank 0's buffer: complete the step
-            for st_ in streams:
-                s.wait_stream(st_)
-            p2p.step_done()
+        if p2p is not None:  # frames stored in rank 0's buffer: device-side completion flags
+            p2p.step_done(step, streams)
             return []
-        # the gather of step k waits for its own views only; the caller's wait() on the
+        # the gather of step k waits for its own views only; the pipeline's wait() on the
         # handles (on s, which every stream waits on at the next step's start) keeps
         # step k + 2 from overwriting this step's frame buffer before it has left
         evs = []
@@ -255,22 +348,22 @@ def run_ours(a, rank, world, local_rank):
         with torch.cuda.stream(comm):
             for e in evs:
                 comm.wait_event(e)
-            return gather_frames(buf, recv[step & 1] if rank == 0 else None, rank, world)
+            return gather_frames(frames[bi], recv[bi] if rank == 0 else None, rank, world)
+
+    def run_steps(first, steps, ev_pairs=None):
+        run_gather_pipeline(first, steps, V, rank, world, n_orbit,
+                            lambda k, views, bi: render_step(k, views, bi, ev_pairs), post_step)
 
     def join():
         for st_ in streams:
             s.wait_stream(st_)
         if comm is not None:
             s.wait_stream(comm)
+        if p2p is not None:
+            p2p.join(s)
 
     # warm-up (also validates capacity)
-    pending = []
-    for w in range(a.warmup):
-        for q in pending:
-            q.wait()
-        pending = step_fn(w)
-    for q in pending:
-        q.wait()
+    run_steps(0, a.warmup)
     join()
     torch.cuda.synchronize()
     st = r.stats()
@@ -278,7 +371,7 @@ def run_ours(a, rank, world, local_rank):
 
     # work counts + frame-level bytes for the views of the timed region (untimed pass)
     work = dict(gauss_tests=0, gauss_frags=0, tri_tests=0, tri_frags=0)
-    bytes_alg = 0.0
+    bytes_alg = bytes_alg_survey = 0.0
     K_sum = 0
     tmp = torch.empty((H, W, 4), dtype=torch.float32, device=dev)
     timed_views = [vi for k in range(a.steps) for vi in views_of(a.warmup + k)]
@@ -291,9 +384,10 @@ def run_ours(a, rank, world, local_rank):
             work[k2] += wk[k2]
         stt = r.stats()
         K_sum += stt["num_pairs"]
-        bytes_alg += alg_bytes(sc.gaussians.count, sc.mesh.num_triangles, sc.mesh.num_vertices,
-                               stt["visible_gaussians"], stt["visible_triangles"],
-                               sc.gaussians.count + sc.mesh.num_triangles, stt["num_pairs"], W, H)
+        args = (sc.gaussians.count, sc.mesh.num_triangles, sc.mesh.num_vertices, stt["visible_gaussians"],
+                stt["visible_triangles"], sc.gaussians.count + sc.mesh.num_triangles, stt["num_pairs"], W, H)
+        bytes_alg += alg_bytes(*args)
+        bytes_alg_survey += alg_bytes_survey(*args)
     torch.cuda.synchronize()
 
     # ---- timed region ---------------------------------------------------------
@@ -307,14 +401,7 @@ def run_ours(a, rank, world, local_rank):
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     blend_ev = []
     t_start.record(s)
-    pending = []
-    for k in range(a.steps):
-        new = step_fn(a.warmup + k, blend_ev)
-        for q in pending:  # frames of step k-1 must have left before buffer k+1 is rewritten
-            q.wait()
-        pending = new
-    for q in pending:
-        q.wait()
+    run_steps(a.warmup, a.steps, blend_ev)
     join()
     t_end.record(s)
     torch.cuda.synchronize()
@@ -385,6 +472,12 @@ def run_ours(a, rank, world, local_rank):
         cpu = {"value": len(times) / sum(times), "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": "views 0 and 128 of the orbit, full 1080p frame each (project + bin + render), "
                          "after one warm-up view"}
+    # ---- per-config single-view numbers, rank 0 at N = 1 only (outside the timed region)
+    configs = None
+    if rank == 0 and world == 1 and not a.no_configs:
+        del ds, rs, r, frames
+        torch.cuda.empty_cache()
+        configs = config_numbers(host_cores())
 
     if rank != 0:
         return
@@ -423,6 +516,7 @@ def run_ours(a, rank, world, local_rank):
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     frame_ms = ms_max / (V * a.steps)
     hbm_gbs = bytes_alg / len(timed_views) / (frame_ms / 1000.0) / 1e9
+    hbm_gbs_survey = bytes_alg_survey / len(timed_views) / (frame_ms / 1000.0) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -432,7 +526,7 @@ def run_ours(a, rank, world, local_rank):
                    "sort_mode": a.sort_mode,
                    "gather": ("none" if not gather else "NCCL send/recv to rank 0" if p2p is None else
                               "fused: blend stores into rank 0's buffer over P2P (CUDA IPC)"),
-                   "l2": "inputs larger than L2 (scene %.2f GB > 126 MB; per-view K ~7.5M pairs)" % (ds.nbytes() / 1e9),
+                   "l2": "inputs larger than L2 (scene %.2f GB > 126 MB; per-view K ~7.5M pairs)" % scene_gb,
                    "parallelism": f"views i mod {world}", "streams_per_gpu": nS,
                    "prio_streams": bool(a.prio), "sort_ctas_per_sm": spm},
         "frame_ms": frame_ms,
@@ -449,10 +543,16 @@ def run_ours(a, rank, world, local_rank):
                                     f"(single-stream pass over the timed views, right after the timed region); "
                                     f"in_region_*: the same events inside the timed region, where each launch "
                                     f"shares the GPU with {nS - 1} other contexts and the high-priority sorts",
-                     "peak_note": f"{sm_count} SMs x 4 schedulers x 32 lanes x 1965 MHz (issue-slot lane-ops)",
+                     "peak_kind": "nominal (not driver-measured): the guide's unit counts x max SM clock",
+                     "peak_note": f"of nominal: {sm_count} SMs x 4 schedulers x 32 lanes x 1965 MHz (issue-slot "
+                                  f"lane-ops); the FFMA micro-benchmark reaches 72.5 TFLOP/s = 36.3 T lane-ops/s",
                      "work_per_launch": {k: v / n_blend for k, v in work.items()}},
         "hbm": {"alg_bytes_per_frame": bytes_alg / len(timed_views), "achieved_gbs": hbm_gbs,
                 "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak,
+                "alg_bytes_note": "DESIGN.md §5: N x 44 + N_vis x 192 (SH of visible Gaussians only) + ...",
+                "survey_alg_bytes_per_frame": bytes_alg_survey / len(timed_views),
+                "survey_achieved_gbs": hbm_gbs_survey, "survey_frac": hbm_gbs_survey / hbm_peak,
+                "survey_note": "SURVEY §8(d) B_alg: N x 236 (every input byte once) + ...",
                 "peak_note": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
         "blend_isolated_over_frame": blend_iso_ms / frame_ms,
         "clocks": clocks.summary(),
@@ -462,6 +562,8 @@ def run_ours(a, rank, world, local_rank):
         "cpu_baseline": cpu,
         "stats_last_view": {k: st[k] for k in ("num_pairs", "visible_gaussians", "visible_triangles",
                                                 "max_tile_pairs")},
+        "world": world_info(world, gather, p2p is not None),
+        "configs": configs,
     }
     print(json.dumps(line), flush=True)
 

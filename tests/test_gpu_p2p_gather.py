@@ -1,9 +1,11 @@
 """The fused P2P frame gather (dist.P2PFrameGather; SURVEY §8(e) variant) on one GPU.
 
 Two processes share the GPU (CUDA IPC works between processes of one device); rank 1's
-blend writes its frames straight into rank 0's buffer through the IPC mapping, the ranks
-meet at a host barrier (no kernel waits on another rank), and rank 0 checks every
-gathered frame bit-for-bit against its own render of the same view.
+blend writes its frames straight into rank 0's buffer through the IPC mapping, steps
+complete through device-side flags (stream memory operations: rank 1 writes done, rank 0
+waits for it and writes free, rank 1 waits for free before reusing a slot -- no host
+barrier, no kernel waits on another rank), and rank 0 checks every gathered frame of the
+last two steps bit-for-bit against its own render of the same view.
 """
 import os
 import socket
@@ -38,13 +40,18 @@ def _worker(rank, world, port, result):
     g = P2PFrameGather(V, c0.height, c0.width, rank, world)
     r = R.renderer_for(sc)
     ds = R.to_device(sc)
-    for step in range(2):
+    s = torch.cuda.current_stream()
+    steps = 5
+    for step in range(steps):  # steps >= 2 reuse a slot: the device-side free flags gate it
+        g.before_step(step, [s])
         for j, vi in enumerate(views_for_rank(step, V, rank, world, len(cams))):
             r.render_view(ds, cams[vi], out=g.frames(step)[j])
-        g.step_done()
+        g.step_done(step, [s])
+    g.join(s)
+    torch.cuda.synchronize()
     ok = True
     if rank == 0:
-        for step in range(2):
+        for step in range(steps - 2, steps):  # the last two steps are still in the buffer
             for src in range(world):
                 for j, vi in enumerate(views_for_rank(step, V, src, world, len(cams))):
                     want = r.render_view(ds, cams[vi]).clone()
