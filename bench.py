@@ -278,15 +278,10 @@ def run_ours(a, rank, world, local_rank):
     # several contexts render concurrently: one sort CTA per SM leaves the rest of
     # each SM to the other contexts' blends (settings.sort_ctas_per_sm)
     spm = a.sort_ctas_per_sm if a.sort_ctas_per_sm >= 0 else (1 if nS > 1 else 0)
-    rs = [R.Renderer(sc.gaussians.count, sc.mesh.num_triangles, 20 << 20, W, H, bg=tuple(float(v) for v in sc.bg),
-                     sort_mode=a.sort_mode, sort_ctas_per_sm=spm) for _ in range(nS)]
+    pool = R.ContextPool(nS, sc.gaussians.count, sc.mesh.num_triangles, 20 << 20, W, H, prio=bool(a.prio),
+                         device=dev, bg=tuple(float(v) for v in sc.bg), sort_mode=a.sort_mode, sort_ctas_per_sm=spm)
+    rs, streams = pool.rs, pool.streams
     r = rs[0]
-    streams = [torch.cuda.Stream(device=dev) for _ in range(nS)]
-    # --prio: each context's preprocess + bin on a high-priority stream, its blend on
-    # the normal one, so the latency-bound sort passes of one view get SMs ahead of
-    # the queued CTAs of another view's compute-bound blend
-    # (torch maps a priority beyond the device's range to its highest priority)
-    pstreams = [torch.cuda.Stream(device=dev, priority=-100) for _ in range(nS)] if a.prio else streams
     ds = R.to_device(sc, dev)
     scene_gb = ds.nbytes() / 1e9
     V = a.views
@@ -311,22 +306,7 @@ def run_ours(a, rank, world, local_rank):
             st_.wait_stream(s)  # (s carries the waits on the gather handles of step - 2)
         if p2p is not None:
             p2p.before_step(step, streams)  # rank 0 has released step - 2's slot (device-side)
-        for j, vi in enumerate(views):
-            rr, ss_, ps_ = rs[j % nS], streams[j % nS], pstreams[j % nS]
-            if ps_ is not ss_:
-                ps_.wait_stream(ss_)  # the context's previous blend has released its buffers
-            rr.preprocess(ds, sc.cameras[vi], stream=ps_)
-            rr.bin(stream=ps_)
-            if ps_ is not ss_:
-                ss_.wait_stream(ps_)
-            if ev_pairs is not None:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(ss_)
-                rr.render(buf[j], stream=ss_)
-                e1.record(ss_)
-                ev_pairs.append((e0, e1))
-            else:
-                rr.render(buf[j], stream=ss_)
+        pool.render_views(ds, [sc.cameras[vi] for vi in views], buf, ev_pairs=ev_pairs)
         # No join at the end of a step: the next step's views queue behind this one's on
         # each context's streams (steps pipeline like the iterations of a serving loop);
         # the timed region joins all streams once, before its end event.
@@ -397,7 +377,7 @@ def run_ours(a, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    launches0 = sum(x.launch_count() for x in rs)
+    launches0 = pool.launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     blend_ev = []
     t_start.record(s)
@@ -408,7 +388,7 @@ def run_ours(a, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     clocks.stop()
-    launches = sum(x.launch_count() for x in rs) - launches0
+    launches = pool.launch_count() - launches0
     ms = t_start.elapsed_time(t_end)
     blend_ms = sum(e0.elapsed_time(e1) for e0, e1 in blend_ev) / max(len(blend_ev), 1)
     t = torch.tensor([ms, blend_ms], dtype=torch.float64, device=dev)
@@ -475,7 +455,7 @@ def run_ours(a, rank, world, local_rank):
     # ---- per-config single-view numbers, rank 0 at N = 1 only (outside the timed region)
     configs = None
     if rank == 0 and world == 1 and not a.no_configs:
-        del ds, rs, r, frames
+        del ds, rs, r, frames, pool
         torch.cuda.empty_cache()
         configs = config_numbers(host_cores())
 

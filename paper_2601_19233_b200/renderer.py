@@ -285,6 +285,56 @@ class Renderer:
         return int(self.L.unimgs_launch_count(self._h))
 
 
+class ContextPool:
+    """Several renderer contexts rendering consecutive views concurrently (the bench's
+    launch configuration): view j of a batch goes to context j % n on its
+    own stream, so the compute-bound blend of one view overlaps the latency-bound
+    binning of the next.  With prio, each context's preprocess + bin run on a
+    highest-priority stream and its blend on the normal one; sort_ctas_per_sm = 1 leaves
+    most of each SM to the other contexts' blends."""
+
+    def __init__(self, n: int, max_gaussians: int, max_triangles: int, max_pairs: int, max_w: int, max_h: int,
+                 prio: bool = True, device=None, **settings):
+        settings.setdefault("sort_ctas_per_sm", 1 if n > 1 else 0)
+        self.rs = [Renderer(max_gaussians, max_triangles, max_pairs, max_w, max_h, **settings) for _ in range(n)]
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(n)]
+        # (torch maps a priority beyond the device's range to its highest priority)
+        self.pstreams = [torch.cuda.Stream(device=device, priority=-100) for _ in range(n)] if prio else self.streams
+
+    def render_views(self, scene: DeviceScene, cams: Sequence[SceneCamera], out: torch.Tensor, after=None,
+                     ev_pairs=None):
+        """Enqueue cams[j] -> out[j] on context j % n.  `after`: a stream every context waits
+        on first.  ev_pairs (list): collects (start, end) CUDA events around each blend.
+        No join at the end: the caller joins `streams` when it needs the frames."""
+        n = len(self.rs)
+        if after is not None:
+            for st in self.streams:
+                st.wait_stream(after)
+        for j, cam in enumerate(cams):
+            rr, ss, ps = self.rs[j % n], self.streams[j % n], self.pstreams[j % n]
+            if ps is not ss:
+                ps.wait_stream(ss)  # the context's previous blend has released its buffers
+            rr.preprocess(scene, cam, stream=ps)
+            rr.bin(stream=ps)
+            if ps is not ss:
+                ss.wait_stream(ps)
+            if ev_pairs is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(ss)
+                rr.render(out[j], stream=ss)
+                e1.record(ss)
+                ev_pairs.append((e0, e1))
+            else:
+                rr.render(out[j], stream=ss)
+
+    def join(self, stream):
+        for st in self.streams:
+            stream.wait_stream(st)
+
+    def launch_count(self) -> int:
+        return sum(r.launch_count() for r in self.rs)
+
+
 def deform(scene: DeviceScene, face: torch.Tensor, bary: torch.Tensor, faces: torch.Tensor, vdata: torch.Tensor,
            stream=None):
     """Eq.12-13 on the device: returns (means' [N,3], cov' [N,6]) CUDA tensors.

@@ -317,37 +317,27 @@ def test_sort_ctas_per_sm_agree(built, mode):
 
 
 def test_multiview_bench_launch_configuration(built, oracle_mod):
-    """The bench's launch configuration at full size: 3M-Gaussian multiview scene,
-    views round-robin on 3 contexts concurrently (bench.py step_fn): one sort CTA
-    per SM, preprocess + bin on high-priority streams, blends on normal ones.
-    Every frame equals the single-context render of its view bit for bit, and one
-    of them matches the oracle on sampled tiles."""
+    """The bench's launch configuration at full size (bench.py's defaults through the same
+    renderer.ContextPool): the 3M-Gaussian multiview scene, views round-robin on 4
+    contexts concurrently, one sort CTA per SM, preprocess + bin on high-priority
+    streams, blends on normal ones, two steps queued back to back without a join.
+    Every frame equals the single-context render of its view bit for bit, and two of
+    them match the oracle on sampled tiles."""
     import torch
     from paper_2601_19233_b200 import renderer as R
     sc = scenes.make_multiview()
     ds = R.to_device(sc)
     cam0 = sc.cameras[0]
     W, H = cam0.width, cam0.height
-    views = [3, 40, 77, 114, 151, 188]
-    nS = 3
-    rs = [R.Renderer(sc.gaussians.count, sc.mesh.num_triangles, 20 << 20, W, H,
-                     bg=tuple(float(v) for v in sc.bg), bg_alpha=float(sc.bg_alpha), sort_ctas_per_sm=1)
-          for _ in range(nS)]
-    streams = [torch.cuda.Stream() for _ in range(nS)]
-    pstreams = [torch.cuda.Stream(priority=-100) for _ in range(nS)]
+    views = [3, 40, 77, 114, 151, 188, 225, 6]
+    pool = R.ContextPool(4, sc.gaussians.count, sc.mesh.num_triangles, 20 << 20, W, H,
+                         bg=tuple(float(v) for v in sc.bg), bg_alpha=float(sc.bg_alpha))
+    assert all(r._settings.sort_ctas_per_sm == 1 for r in pool.rs)
     out = torch.empty((len(views), H, W, 4), device="cuda")
     s = torch.cuda.current_stream()
-    for st_ in streams:
-        st_.wait_stream(s)
-    for j, vi in enumerate(views):
-        rr, ss_, ps_ = rs[j % nS], streams[j % nS], pstreams[j % nS]
-        ps_.wait_stream(ss_)
-        rr.preprocess(ds, sc.cameras[vi], stream=ps_)
-        rr.bin(stream=ps_)
-        ss_.wait_stream(ps_)
-        rr.render(out[j], stream=ss_)
-    for st_ in streams:
-        s.wait_stream(st_)
+    pool.render_views(ds, [sc.cameras[v] for v in views[:4]], out[:4], after=s)
+    pool.render_views(ds, [sc.cameras[v] for v in views[4:]], out[4:])  # the next step, no join
+    pool.join(s)
     torch.cuda.synchronize()
     single = R.Renderer(sc.gaussians.count, sc.mesh.num_triangles, 20 << 20, W, H,
                         bg=tuple(float(v) for v in sc.bg), bg_alpha=float(sc.bg_alpha))
@@ -355,11 +345,12 @@ def test_multiview_bench_launch_configuration(built, oracle_mod):
         ref = single.render_view(ds, sc.cameras[vi])
         torch.cuda.synchronize()
         assert torch.equal(out[j], ref), vi
-    o = oracle_mod.Oracle(sc.gaussians, sc.mesh)
-    o.project(sc.cameras[views[1]], **oracle_mod.scene_settings(sc))
-    o.bin()
-    tiles = np.random.default_rng(2).choice(o.tiles_x * o.tiles_y, 300, replace=False)
-    compare_image(out[1].cpu().numpy(), o.render(tiles))
+    for j in (1, 6):
+        o = oracle_mod.Oracle(sc.gaussians, sc.mesh)
+        o.project(sc.cameras[views[j]], **oracle_mod.scene_settings(sc))
+        o.bin()
+        tiles = np.random.default_rng(2 + j).choice(o.tiles_x * o.tiles_y, 300, replace=False)
+        compare_image(out[j].cpu().numpy(), o.render(tiles))
 
 
 def test_8k_image_full_keys(built, oracle_mod):
