@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("UNIMGS_LIB", os.path.join(HERE, "libunimgs.so"))  # override: experiments only
+LIB_PATH = os.environ.get("UNIMGS_LIB") or os.path.join(HERE, "libunimgs.so")  # override: experiments only
 
 OK, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED, ERR_CAPACITY, ERR_CUDA, ERR_STATE = range(6)
 STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "UNSUPPORTED", 3: "CAPACITY", 4: "CUDA", 5: "STATE"}

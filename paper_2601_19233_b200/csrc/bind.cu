@@ -8,7 +8,7 @@
 //
 //   k_centroid_bounds  scene box of the face centroids (ordered-int atomics)
 //   k_morton           30-bit Morton code per valid face (invalid: 0xFFFFFFFF)
-//   cub radix sort     (code, face) pairs -- a library sort in a one-time build
+//   onesweep sort      (code, face) pairs, stable LSD (binning.cu's depth-sort kernels)
 //                      (not on the per-frame path); invalid faces sort last
 //   k_karras           internal nodes of the radix tree (Karras 2012): ranges
 //                      and splits from common-prefix lengths, ties by index
@@ -24,7 +24,6 @@
 // prunes with padded boxes and t_near > best t, and ties go to the lower face
 // id, so the result does not depend on the visiting order: it equals the
 // exhaustive search.
-#include <cub/cub.cuh>
 
 #include "internal.cuh"
 
@@ -390,9 +389,9 @@ int launch_bind(const BindInput &in, int32_t *face_out, float *bary_out, double 
     const int64_t Fa = F > 0 ? F : 1;
     int launches = 0;
     BvhScratch b{};
-    size_t sort_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (uint32_t *)nullptr, (uint32_t *)nullptr, (int)Fa, 0, 32, s);
+    // the sort's scratch: a DevState (n_vis = F) and the look-back rows, both zeroed
+    const int64_t lb_rows = sort_lookback_tiles(Fa, Fa);
+    const size_t sort_bytes = sizeof(DevState) + 256 + (size_t)lb_rows * 256 * sizeof(unsigned long long);
     // one stream-ordered scratch block
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t nb = 2 * (size_t)Fa;
@@ -424,18 +423,27 @@ int launch_bind(const BindInput &in, int32_t *face_out, float *bary_out, double 
         k_centroid_bounds<<<blocks, 256, 0, s>>>(F, in.V, in.pos, in.faces, b.bounds);
         k_morton<<<(unsigned)((F + 255) / 256), 256, 0, s>>>(F, in.V, in.pos, in.faces, b.bounds, b.code[0],
                                                              b.face[0]);
-        cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, b.code[0], b.code[1], b.face[0], b.face[1], (int)F, 0,
-                                        32, s);  // invalid faces (code 0xFFFFFFFF) last
-        k_karras<<<(unsigned)((F + 255) / 256), 256, 0, s>>>(b.bounds, b.code[1], b.child, b.parent);
-        k_leaf_boxes<<<(unsigned)((F + 255) / 256), 256, 0, s>>>(b.bounds, in.V, in.pos, in.faces, b.face[1], b.child,
+        {   // stable sort of (code, face); invalid faces (code 0xFFFFFFFF) last
+            DevState *st = reinterpret_cast<DevState *>(sort_tmp);
+            unsigned long long *lb = reinterpret_cast<unsigned long long *>(static_cast<char *>(sort_tmp) +
+                                                                           al(sizeof(DevState)));
+            cudaMemsetAsync(sort_tmp, 0, sort_bytes, s);
+            const unsigned n32 = (unsigned)F;
+            cudaMemcpyAsync(&st->n_vis, &n32, sizeof n32, cudaMemcpyHostToDevice, s);
+            int dev = 0, sms = 148;
+            if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            launches += launch_sort_u32_pairs(b.code, b.face, F, st, lb, sms, s);  // result in code[0] / face[0]
+        }
+        k_karras<<<(unsigned)((F + 255) / 256), 256, 0, s>>>(b.bounds, b.code[0], b.child, b.parent);
+        k_leaf_boxes<<<(unsigned)((F + 255) / 256), 256, 0, s>>>(b.bounds, in.V, in.pos, in.faces, b.face[0], b.child,
                                                                  b.parent, b.arrive, b.lo, b.hi);
-        launches += 5;
+        launches += 4;
     }
     const int K = in.mode == 0 ? 1 : 8;
     const int64_t threads = in.N * K;
     if (threads > 0) {
         TraceArgs A{in.N,  in.means, in.quats, in.scales, in.mode,  in.k_sigma, in.ncams,  cams,      in.V,
-                    in.pos, in.faces, b.bounds, b.child,   b.lo,     b.hi,       b.face[1], face_out, bary_out,
+                    in.pos, in.faces, b.bounds, b.child,   b.lo,     b.hi,       b.face[0], face_out, bary_out,
                     dist2_out};
         k_bind_trace<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(A);
         launches++;

@@ -677,8 +677,9 @@ static int bits_for(int64_t tiles) {
 }
 
 template <typename KT, int ITEMS, int NB>
-static void onesweep_launch(Buffers &b, const KT *kin, const uint32_t *vin, KT *kout, uint32_t *vout,
-                            const unsigned *n_ptr, int shift, int hist_row, int slot, int grid, cudaStream_t s) {
+static void onesweep_launch(DevState *st, unsigned long long *lookback, const KT *kin, const uint32_t *vin, KT *kout,
+                            uint32_t *vout, const unsigned *n_ptr, int shift, int hist_row, int slot, int grid,
+                            cudaStream_t s) {
     static const bool attr = [] {  // dynamic shared memory above 48 KB, once per instantiation (thread-safe)
         cudaFuncSetAttribute(k_onesweep<KT, ITEMS, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)onesweep_smem<KT, ITEMS>());
@@ -686,14 +687,15 @@ static void onesweep_launch(Buffers &b, const KT *kin, const uint32_t *vin, KT *
     }();
     (void)attr;
     k_onesweep<KT, ITEMS, NB><<<grid, kSortThreads, onesweep_smem<KT, ITEMS>(), s>>>(
-        kin, vin, kout, vout, n_ptr, shift, &b.st->hist[hist_row][0], slot, b.lookback, b.st);
+        kin, vin, kout, vout, n_ptr, shift, &st->hist[hist_row][0], slot, lookback, st);
 }
 
 template <typename KT, int ITEMS = kSortItems>
 static void onesweep_pass(Buffers &b, const KT *kin, const uint32_t *vin, KT *kout, uint32_t *vout,
                           const unsigned *n_ptr, int shift, int bits, int hist_row, int slot, int grid,
                           cudaStream_t s) {
-#define UNIMGS_OS(NB) onesweep_launch<KT, ITEMS, NB>(b, kin, vin, kout, vout, n_ptr, shift, hist_row, slot, grid, s)
+#define UNIMGS_OS(NB) \
+    onesweep_launch<KT, ITEMS, NB>(b.st, b.lookback, kin, vin, kout, vout, n_ptr, shift, hist_row, slot, grid, s)
     switch (bits) {
         case 1: UNIMGS_OS(1); break;
         case 2: UNIMGS_OS(2); break;
@@ -836,6 +838,22 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
     k_tile_order<<<1, 1024, 0, s>>>(b.ranges, (int)tiles, b.order, b.st);
     launches++;
     return launches;  // kernels only (the ranges memset is not counted)
+}
+
+// Stable LSD sort of n (u32 key, u32 value) pairs, 4 x 8-bit onesweep passes with the
+// depth-sort kernels (the ray-cast binding's Morton codes, bind.cu): keys[0]/vals[0] in,
+// result back in keys[0]/vals[0] (keys[1]/vals[1] scratch).  st: a zeroed DevState whose
+// n_vis holds n; lookback: zeroed [sort_lookback_tiles(n, n)][256].
+int launch_sort_u32_pairs(uint32_t *keys[2], uint32_t *vals[2], int64_t n, DevState *st, unsigned long long *lookback,
+                          int sm_count, cudaStream_t s) {
+    if (n <= 0) return 0;
+    k_hist_depth<<<sm_count * 2, 256, 0, s>>>(keys[0], st);
+    const int grid = sort_grid(n, sm_count, 4, kSortThreads * kDepthItems);
+    for (int pass = 0; pass < 4; pass++)
+        onesweep_launch<uint32_t, kDepthItems, 8>(st, lookback, keys[pass & 1], vals[pass & 1], keys[(pass & 1) ^ 1],
+                                                  vals[(pass & 1) ^ 1], &st->n_vis, 8 * pass, HIST_DEPTH0 + pass,
+                                                  SLOT_PASS0 + pass, grid, s);
+    return 5;
 }
 
 // ---- debug / stats ------------------------------------------------------------

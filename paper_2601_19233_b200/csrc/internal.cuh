@@ -169,5 +169,9 @@ int launch_deform(const DeformInput &d, float *mu_out, float *cov_out, cudaStrea
 // ray-cast binding (bind.cu): builds an LBVH in stream-ordered scratch; -1 if that allocation fails
 int launch_bind(const BindInput &in, int32_t *face_out, float *bary_out, double *dist2_out, cudaStream_t s);
 int launch_full_keys(const Buffers &b, uint64_t *keys, cudaStream_t s);
+// stable LSD sort of (u32 key, u32 value) pairs in keys[0]/vals[0] (binning.cu's onesweep);
+// st zeroed with n_vis = n, lookback zeroed with sort_lookback_tiles(n, n) rows
+int launch_sort_u32_pairs(uint32_t *keys[2], uint32_t *vals[2], int64_t n, DevState *st, unsigned long long *lookback,
+                          int sm_count, cudaStream_t s);
 
 }  // namespace unimgs
