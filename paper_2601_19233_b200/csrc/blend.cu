@@ -518,18 +518,21 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
                     ec[k] = wb.col[2 * p + k];
                     al[k] = fminf(bp.alpha_max, ex2_ftz(fmaf(q[k], kexp, ec[k].w)));
                 }
+                f32x2 c01 = pk2(s.C0, s.C1);  // (R, G) accumulated as one f32x2 FFMA2
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
                     // (entry 0: a pixel already done has q = NaN, so no T test is needed)
                     const bool h = q[k] <= m[k] && (k == 0 || s.T >= bp.t_eps);
                     const float w = h ? s.T * al[k] : 0.f;
-                    s.C0 += w * ec[k].x; s.C1 += w * ec[k].y; s.C2 += w * ec[k].z;
+                    c01 = fma2(pk2(w, w), pk2(ec[k].x, ec[k].y), c01);
+                    s.C2 += w * ec[k].z;
                     s.T -= w;  // a fragment closes an open entity: T != Tlast
                     if (COUNT && h) {
                         w_gf++;
                         last_id = s_ids[COUNT ? warp : 0][2 * p + k];
                     }
                 }
+                upk2(c01, s.C0, s.C1);
                 if (s.T < bp.t_eps) s.finish();
             }
         } else if (!has_tri) {
