@@ -182,7 +182,7 @@ extern "C" int unimgs_set_settings(unimgs_ctx *c, const unimgs_settings *s) {
 static void free_buffers(unimgs_ctx *c) {
     Buffers &b = c->buf;
     void *ptrs[] = {b.rect, b.touched, b.dkey, b.grec, b.trec, b.pk[0], b.pk[1], b.pv[0], b.pv[1], b.tk[0], b.tk[1],
-                    b.tv[0], b.tv[1], b.ranges, b.order, b.bcnt, b.dcnt, b.rstart, b.lookback, b.st};
+                    b.tv[0], b.tv[1], b.ranges, b.order, b.bcnt, b.dcnt, b.rstart, b.lookback, b.tcnt, b.gsum, b.st};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     memset(&b, 0, sizeof b);
@@ -221,6 +221,8 @@ extern "C" int unimgs_reserve2(unimgs_ctx *c, int64_t max_gaussians, int64_t max
     CUDA_TRY(c, dev_alloc(c, &b.dcnt, sizeof(uint32_t) * (size_t)(P / 2048 + 4)));
     CUDA_TRY(c, dev_alloc(c, &b.rstart, sizeof(uint32_t) * (size_t)n_rstart));
     CUDA_TRY(c, dev_alloc(c, &b.lookback, sizeof(unsigned long long) * 256 * lb_tiles));
+    CUDA_TRY(c, dev_alloc(c, &b.tcnt, sizeof(uint32_t) * 256 * lb_tiles));
+    CUDA_TRY(c, dev_alloc(c, &b.gsum, sizeof(uint32_t) * 256 * (lb_tiles / 32 + 3)));
     CUDA_TRY(c, dev_alloc(c, &b.st, sizeof(DevState)));
     CUDA_TRY(c, cudaMemset(b.lookback, 0, sizeof(unsigned long long) * 256 * lb_tiles));
     CUDA_TRY(c, cudaMemset(b.st, 0, sizeof(DevState)));

@@ -337,7 +337,8 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
                                                          const uint32_t *__restrict__ prel,
                                                          const uint32_t *__restrict__ rstart, int tiles_x,
                                                          const TriRecord *__restrict__ trec, unsigned F, int tri_depth,
-                                                         int lo_bits, void *tk_, uint32_t *tv, DevState *st) {
+                                                         int lo_bits, void *tk_, uint32_t *tv, uint32_t *tcnt,
+                                                         DevState *st) {
     using Key = typename DupCfg<FULL>::Key;
     constexpr int SLOTS = ExpandCfg<FULL>::SLOTS, PER = ExpandCfg<FULL>::PER, MP = SLOTS + 2;
     __shared__ int s_off[MP];          // primitive start slot relative to the range (first may be < 0)
@@ -368,6 +369,8 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
         const int m = (int)(p1 - p0) + 1;
         UNIMGS_CHECK(m >= 1 && m + 1 <= MP && p1 < n);
         __syncthreads();  // previous range's staging consumed
+        if (!FULL)  // sort_mode 0: the range is one sort tile; its low-digit counts, per range
+            for (int i = threadIdx.x; i < 256; i += kScanThreads) s_hl[i] = 0;
         for (int j = threadIdx.x; j < m; j += kScanThreads) {
             const unsigned i = p0 + j;
             const uint32_t id = ids[i];
@@ -412,7 +415,7 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
                 s_v[k] = pid;
                 // sort_mode 0 splits the tile id into lo_bits + the rest (balanced digits)
                 atomicAdd(&s_hl[FULL ? t & 255u : t & ((1u << lo_bits) - 1u)], 1u);
-                atomicAdd(&s_hh[FULL ? (t >> 8) & 255u : (t >> lo_bits) & 255u], 1u);
+                if (FULL) atomicAdd(&s_hh[FULL ? (t >> 8) & 255u : 0], 1u);
                 if (FULL) {
                     if (t >= 65536u) atomicAdd(&s_h3[FULL ? (t >> 16) & 255u : 0], 1u);
                     else n_h3_zero++;  // third tile digit 0, added once per thread below
@@ -424,8 +427,11 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
             tk[S + k] = s_k[k];
             tv[S + k] = s_v[k];
         }
+        if (!FULL)
+            for (int i = threadIdx.x; i < 256; i += kScanThreads) tcnt[(size_t)r * 256 + i] = s_hl[i];
     }
     if (FULL && n_h3_zero) atomicAdd(&s_h3[0], n_h3_zero);
+    if (!FULL) return;  // sort_mode 0: the reduce-then-scan tile sort needs no global histograms
     __syncthreads();
     for (int i = threadIdx.x; i < 256; i += kScanThreads) {
         if (s_hl[i]) atomicAdd(&st->hist[FULL ? 4 : HIST_TILE0][i], s_hl[i]);
@@ -603,6 +609,230 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
             kout[o] = kk;
             vout[o] = s_v[k];
         }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Reduce-then-scan LSD pass over the u16 tile keys (sort_mode 0): no decoupled
+// look-back, so no sort tile waits on another (the onesweep chain's spinning was
+// ~40% of a tile pass's instructions).  Per pass:
+//   counts   per sort tile (kSortTile keys) and digit: tcnt[tile][d] -- written by
+//            k_expand for the first pass, by k_tile_count for the second;
+//   scan A   per group of kRtsGroup sort tiles: tcnt := exclusive prefix within the
+//            group, gsum[group][d] := the group's total;
+//   scan B   one CTA: gsum := exclusive prefix over groups, and the digit totals
+//            in gsum row `ngroups_max` (the histogram the downsweep scans);
+//   down     per sort tile: the onesweep ranking (stable warp multisplit), then
+//            global position = exclusive(totals)[d] + gsum[group][d] + tcnt[tile][d]
+//            + the key's rank within the tile.
+// ----------------------------------------------------------------------------
+constexpr int kRtsGroup = 32;
+
+template <int NB>
+__global__ void __launch_bounds__(256) k_tile_count(const uint16_t *__restrict__ keys, const unsigned *n_ptr, int shift,
+                                                    uint32_t *tcnt, const DevState *st) {
+    __shared__ unsigned h[256];
+    if (st->overflow) return;
+    const unsigned n = *n_ptr;
+    for (unsigned tile = blockIdx.x; (unsigned long long)tile * kSortTile < n; tile += gridDim.x) {
+    const unsigned base = tile * (unsigned)kSortTile;
+    __syncthreads();
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    constexpr unsigned mask = (1u << NB) - 1u;
+    const unsigned i0 = base + 8 * threadIdx.x;  // 8 keys per thread, one 16-byte load
+    if (i0 + 8 <= n) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(keys + i0));
+        const unsigned w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            atomicAdd(&h[((w[j] & 0xFFFFu) >> shift) & mask], 1u);
+            atomicAdd(&h[((w[j] >> 16) >> shift) & mask], 1u);
+        }
+    } else {
+        for (unsigned i = i0; i < n && i < i0 + 8; i++) atomicAdd(&h[((unsigned)keys[i] >> shift) & mask], 1u);
+    }
+    __syncthreads();
+    tcnt[(size_t)tile * 256 + threadIdx.x] = h[threadIdx.x];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_rts_scan_a(uint32_t *tcnt, uint32_t *gsum, const unsigned *n_ptr,
+                                                    const DevState *st) {
+    if (st->overflow) return;
+    const unsigned ntiles = (*n_ptr + kSortTile - 1) / kSortTile;
+    const unsigned t0 = blockIdx.x * kRtsGroup;
+    if (t0 >= ntiles) return;
+    const unsigned t1 = min(ntiles, t0 + kRtsGroup), d = threadIdx.x;
+    unsigned c[kRtsGroup];
+#pragma unroll
+    for (int i = 0; i < kRtsGroup; i++) c[i] = t0 + i < t1 ? tcnt[(size_t)(t0 + i) * 256 + d] : 0u;
+    unsigned run = 0;
+#pragma unroll
+    for (int i = 0; i < kRtsGroup; i++) {
+        if (t0 + i < t1) tcnt[(size_t)(t0 + i) * 256 + d] = run;
+        run += c[i];
+    }
+    gsum[(size_t)blockIdx.x * 256 + d] = run;
+}
+
+// 1024 threads: digit d = threadIdx % 256, part q = threadIdx / 256 scans a quarter
+// of the groups; the four partial sums are combined through shared memory.
+__global__ void __launch_bounds__(1024) k_rts_scan_b(uint32_t *gsum, const unsigned *n_ptr, int totals_row,
+                                                     const DevState *st) {
+    __shared__ unsigned s_part[4][256];
+    if (st->overflow) return;
+    const unsigned ntiles = (*n_ptr + kSortTile - 1) / kSortTile;
+    const unsigned ng = (ntiles + kRtsGroup - 1) / kRtsGroup;
+    const unsigned d = threadIdx.x & 255u, q = threadIdx.x >> 8;
+    const unsigned per = (ng + 3) / 4, g0 = q * per, g1 = min(ng, g0 + per);
+    unsigned sum = 0;
+    for (unsigned g = g0; g < g1; g += 8) {
+        unsigned v[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) v[j] = g + j < g1 ? gsum[(size_t)(g + j) * 256 + d] : 0u;
+#pragma unroll
+        for (int j = 0; j < 8; j++) sum += v[j];
+    }
+    s_part[q][d] = sum;
+    __syncthreads();
+    unsigned run = 0;
+    for (unsigned k = 0; k < q; k++) run += s_part[k][d];
+    for (unsigned g = g0; g < g1; g += 8) {
+        unsigned v[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) v[j] = g + j < g1 ? gsum[(size_t)(g + j) * 256 + d] : 0u;
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            if (g + j < g1) {
+                gsum[(size_t)(g + j) * 256 + d] = run;
+                run += v[j];
+            }
+    }
+    if (q == 3) gsum[(size_t)totals_row * 256 + d] = run;  // digit total
+}
+
+template <int ITEMS, int NB>
+__global__ void __launch_bounds__(kSortThreads, UNIMGS_SORT_MINB) k_downsweep(const uint16_t *__restrict__ kin,
+                                                                           const uint32_t *__restrict__ vin,
+                                                                           uint16_t *__restrict__ kout,
+                                                                           uint32_t *__restrict__ vout,
+                                                                           const unsigned *n_ptr, int shift,
+                                                                           const uint32_t *__restrict__ tcnt,
+                                                                           const uint32_t *__restrict__ gsum,
+                                                                           int totals_row, const DevState *st) {
+    using KT = uint16_t;
+    constexpr int TILE_ = kSortThreads * ITEMS;
+    static_assert(TILE_ == kSortTile, "one count row per sort tile");
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned *s_wh = reinterpret_cast<unsigned *>(smem);           // [8][256]
+    unsigned *s_doff = s_wh + 8 * 256;                              // [256] block-local digit offsets
+    int *s_glob = reinterpret_cast<int *>(s_doff + 256);            // [256] global base - local offset
+    unsigned *s_hex = reinterpret_cast<unsigned *>(s_glob + 256);   // [256] global exclusive digit offsets
+    unsigned *s_misc = s_hex + 256;                                 // [16]
+    KT *s_k = reinterpret_cast<KT *>(s_misc + 16);
+    uint32_t *s_v = reinterpret_cast<uint32_t *>(s_k + TILE_);
+    if (st->overflow) return;
+    const unsigned n = *n_ptr;
+    constexpr unsigned mask = (1u << NB) - 1u;
+    const unsigned t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    unsigned hex;
+    {   // exclusive scan of the digit totals, 1 digit per thread
+        const unsigned h = gsum[(size_t)totals_row * 256 + t];
+        unsigned x = h;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (unsigned)o) x += y;
+        }
+        if (lane == 31) s_misc[8 + wid] = x;
+        __syncthreads();
+        unsigned add = 0;
+        for (unsigned w = 0; w < wid; w++) add += s_misc[8 + w];
+        hex = x - h + add;
+    }
+    // persistent: sort tiles are independent (no look-back), so a fixed stride suffices
+    for (unsigned tile = blockIdx.x; (unsigned long long)tile * TILE_ < n; tile += gridDim.x) {
+    const unsigned base = tile * (unsigned)TILE_;
+    __syncthreads();  // the previous tile's shared state consumed
+    for (int i = t; i < 8 * 256; i += kSortThreads) s_wh[i] = 0;
+    s_hex[t] = hex + gsum[(size_t)(tile / kRtsGroup) * 256 + t] + tcnt[(size_t)tile * 256 + t];
+    __syncthreads();
+    KT key[ITEMS];
+    uint32_t val[ITEMS];
+    unsigned rank[ITEMS];
+    const unsigned wbase = base + wid * 32u * ITEMS + lane;
+    const unsigned lt = lanemask_lt();
+    unsigned *wh = s_wh + wid * 256;
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        const unsigned idx = wbase + 32u * i;
+        const bool valid = idx < n;
+        key[i] = valid ? kin[idx] : (KT)0;
+        val[i] = valid ? vin[idx] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        const bool valid = wbase + 32u * i < n;
+        const unsigned d = valid ? (unsigned)((key[i] >> shift) & mask) : 0u;
+        unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int bt = 0; bt < NB; bt++)
+            asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+                "and.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
+                "vote.sync.ballot.b32 t, p, 0xffffffff;\n\t"
+                "@!p not.b32 t, t;\n\tand.b32 %0, %0, t;\n\t}"
+                : "+r"(peers)
+                : "r"(d), "r"(1u << bt));
+        const unsigned before = valid ? wh[d] : 0u;
+        __syncwarp();
+        if (valid && (peers & lt) == 0) wh[d] = before + __popc(peers);
+        __syncwarp();
+        rank[i] = before + __popc(peers & lt);
+    }
+    __syncthreads();
+    unsigned cnt = 0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+        const unsigned c = s_wh[w * 256 + t];
+        s_wh[w * 256 + t] = cnt;
+        cnt += c;
+    }
+    {   // block-exclusive scan of cnt over digits
+        unsigned x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (unsigned)o) x += y;
+        }
+        if (lane == 31) s_misc[8 + wid] = x;
+        __syncthreads();
+        unsigned add = 0;
+        for (unsigned w = 0; w < wid; w++) add += s_misc[8 + w];
+        s_doff[t] = x - cnt + add;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        if (wbase + 32u * i < n) {
+            const unsigned d = (unsigned)((key[i] >> shift) & mask);
+            const unsigned pos = s_doff[d] + wh[d] + rank[i];
+            UNIMGS_CHECK(pos < (unsigned)TILE_);
+            s_k[pos] = key[i];
+            s_v[pos] = val[i];
+        }
+    }
+    s_glob[t] = (int)s_hex[t] - (int)s_doff[t];
+    __syncthreads();
+    const unsigned nt = min((unsigned)TILE_, n - base);
+    for (unsigned k = t; k < nt; k += kSortThreads) {
+        const KT kk = s_k[k];
+        const unsigned d = (unsigned)((kk >> shift) & mask);
+        const unsigned o = (unsigned)(s_glob[d] + (int)k);
+        UNIMGS_CHECK(o < n);
+        kout[o] = kk;
+        vout[o] = s_v[k];
+    }
     }
 }
 
@@ -804,22 +1034,53 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         // 2048-key sort tile, so longer runs in each pass's scatter
         const int npass = (tb + 7) / 8, lo_bits = npass > 1 ? (tb + npass - 1) / npass : std::max(tb, 1);
         k_expand<false><<<egrid, kScanThreads, 0, s>>>(dup_ids, b.rect, b.dkey, b.dcnt, prel, b.rstart, cam.tiles_x,
-                                                        b.trec, (unsigned)F, 0, lo_bits, b.tk[0], b.tv[0], b.st);
+                                                        b.trec, (unsigned)F, 0, lo_bits, b.tk[0], b.tv[0], b.tcnt,
+                                                        b.st);
         launches++;
+        // reduce-then-scan passes (k_expand wrote the first pass's per-tile counts)
+        const int ntile_max = (int)((b.max_pairs + kSortTile - 1) / kSortTile);
+        const int ngroup_max = (ntile_max + kRtsGroup - 1) / kRtsGroup;
         for (int pass = 0, sh = 0; sh < tb; pass++, slot++) {
             const int nb = pass == 0 ? lo_bits : tb - sh;
-            onesweep_pass<uint16_t>(b, (const uint16_t *)b.tk[tc], b.tv[tc], (uint16_t *)b.tk[tc ^ 1], b.tv[tc ^ 1],
-                                    &b.st->K, sh, nb, HIST_TILE0 + pass, slot, g2, s);
+            const uint16_t *kin = (const uint16_t *)b.tk[tc];
+#define UNIMGS_NB_SWITCH(CALL)  \
+    switch (nb) {               \
+        case 1: CALL(1); break; \
+        case 2: CALL(2); break; \
+        case 3: CALL(3); break; \
+        case 4: CALL(4); break; \
+        case 5: CALL(5); break; \
+        case 6: CALL(6); break; \
+        case 7: CALL(7); break; \
+        default: CALL(8); break; \
+    }
+            if (pass > 0) {
+#define UNIMGS_TC(NB) k_tile_count<NB><<<std::min(ntile_max, sm_count * 8), 256, 0, s>>>(kin, &b.st->K, sh, b.tcnt, b.st)
+                UNIMGS_NB_SWITCH(UNIMGS_TC)
+#undef UNIMGS_TC
+                launches++;
+            }
+            k_rts_scan_a<<<ngroup_max, 256, 0, s>>>(b.tcnt, b.gsum, &b.st->K, b.st);
+            k_rts_scan_b<<<1, 1024, 0, s>>>(b.gsum, &b.st->K, ngroup_max, b.st);
+            const size_t smem = onesweep_smem<uint16_t, kSortItems>();
+#define UNIMGS_DS(NB)                                                                                          \
+    k_downsweep<kSortItems, NB><<<g2, kSortThreads, smem, s>>>(kin, b.tv[tc], (uint16_t *)b.tk[tc ^ 1],        \
+                                                                      b.tv[tc ^ 1], &b.st->K, sh, b.tcnt, b.gsum, \
+                                                                      ngroup_max, b.st)
+            UNIMGS_NB_SWITCH(UNIMGS_DS)
+#undef UNIMGS_DS
+#undef UNIMGS_NB_SWITCH
+            launches += 3;
             sh += nb;
             tc ^= 1;
-            launches++;
         }
         b.key_bytes = 2;
         k_ranges16<<<sm_count * 4, 256, 0, s>>>((const uint16_t *)b.tk[tc], &b.st->K, b.ranges, b.st);
         launches++;
     } else {
         k_expand<true><<<egrid, kScanThreads, 0, s>>>(dup_ids, b.rect, b.dkey, b.dcnt, prel, b.rstart, cam.tiles_x,
-                                                       b.trec, (unsigned)F, tri_depth, 8, b.tk[0], b.tv[0], b.st);
+                                                       b.trec, (unsigned)F, tri_depth, 8, b.tk[0], b.tv[0], nullptr,
+                                                       b.st);
         launches++;
         const int total_bits = 32 + tb;
         for (int pass = 0, sh = 0; sh < total_bits; pass++, sh += 8, slot++) {

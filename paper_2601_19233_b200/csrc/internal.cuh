@@ -94,6 +94,8 @@ struct Buffers {
     uint32_t *dcnt;       // per-CTA pair counts of the duplication (2048 primitives each), scanned in place
     uint32_t *rstart;     // [max_pairs / 1024 + 2] first primitive of each expansion range (k_range_starts)
     unsigned long long *lookback;  // [max_lb_tiles][256]
+    uint32_t *tcnt;       // [max_lb_tiles][256] per sort tile (2048 pairs) digit counts -> exclusive within group
+    uint32_t *gsum;       // [max_lb_tiles / 32 + 2][256] per group of 32 sort tiles -> exclusive; then totals
     DevState *st;
     int64_t max_prims, max_pairs, max_tiles, max_lb_tiles;
     const uint32_t *sorted_vals;   // final per-tile lists (points into tv[*])
