@@ -55,7 +55,7 @@ constexpr int kSortThreads = 256, kSortItems = UNIMGS_SORT_ITEMS, kSortTile = kS
 constexpr int kLookWin = UNIMGS_LOOKWIN;  // predecessors inspected per look-back round trip
 
 // scan/pass slots (select the dynamic tile counter and the epoch tag)
-enum { SLOT_COMPACT = 0, SLOT_DUP = 1, SLOT_PASS0 = 2 };
+enum { SLOT_COMPACT = 0, SLOT_DUP = 1, SLOT_PASS0 = 2, SLOT_RTS0 = 12 };  // ctr[16]
 // histogram rows: 0..3 depth digits, 4..5 tile digits (weighted by pairs in mode 1)
 enum { HIST_DEPTH0 = 0, HIST_TILE0 = 4 };
 
@@ -618,10 +618,10 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
 // ~40% of a tile pass's instructions).  Per pass:
 //   counts   per sort tile (kSortTile keys) and digit: tcnt[tile][d] -- written by
 //            k_expand for the first pass, by k_tile_count for the second;
-//   scan A   per group of kRtsGroup sort tiles: tcnt := exclusive prefix within the
-//            group, gsum[group][d] := the group's total;
-//   scan B   one CTA: gsum := exclusive prefix over groups, and the digit totals
-//            in gsum row `ngroups_max` (the histogram the downsweep scans);
+//   scan     per group of kRtsGroup sort tiles: tcnt := exclusive prefix within the
+//            group, gsum[group][d] := the group's total; the last CTA to finish
+//            then makes gsum the exclusive prefix over groups and writes the digit
+//            totals into gsum row `ngroups_max` (the histogram the downsweep scans);
 //   down     per sort tile: the onesweep ranking (stable warp multisplit), then
 //            global position = exclusive(totals)[d] + gsum[group][d] + tcnt[tile][d]
 //            + the key's rank within the tile.
@@ -665,10 +665,14 @@ __global__ void __launch_bounds__(256) k_tile_count(const KT *__restrict__ keys,
     }
 }
 
-__global__ void __launch_bounds__(256) k_rts_scan_a(uint32_t *tcnt, uint32_t *gsum, const unsigned *n_ptr,
-                                                    const DevState *st) {
+// Scan A, and -- in the last CTA to finish (threadfence + counter in DevState::ctr[slot])
+// -- scan B over the group sums, so one launch scans a pass's counts.
+__global__ void __launch_bounds__(256) k_rts_scan(uint32_t *tcnt, uint32_t *gsum, const unsigned *n_ptr, int totals_row,
+                                                  int slot, DevState *st) {
+    __shared__ bool s_last;
     if (st->overflow) return;
     const unsigned ntiles = (*n_ptr + kSortTile - 1) / kSortTile;
+    const unsigned ng = (ntiles + kRtsGroup - 1) / kRtsGroup;
     const unsigned t0 = blockIdx.x * kRtsGroup;
     if (t0 >= ntiles) return;
     const unsigned t1 = min(ntiles, t0 + kRtsGroup), d = threadIdx.x;
@@ -682,42 +686,26 @@ __global__ void __launch_bounds__(256) k_rts_scan_a(uint32_t *tcnt, uint32_t *gs
         run += c[i];
     }
     gsum[(size_t)blockIdx.x * 256 + d] = run;
-}
-
-// 1024 threads: digit d = threadIdx % 256, part q = threadIdx / 256 scans a quarter
-// of the groups; the four partial sums are combined through shared memory.
-__global__ void __launch_bounds__(1024) k_rts_scan_b(uint32_t *gsum, const unsigned *n_ptr, int totals_row,
-                                                     const DevState *st) {
-    __shared__ unsigned s_part[4][256];
-    if (st->overflow) return;
-    const unsigned ntiles = (*n_ptr + kSortTile - 1) / kSortTile;
-    const unsigned ng = (ntiles + kRtsGroup - 1) / kRtsGroup;
-    const unsigned d = threadIdx.x & 255u, q = threadIdx.x >> 8;
-    const unsigned per = (ng + 3) / 4, g0 = q * per, g1 = min(ng, g0 + per);
-    unsigned sum = 0;
-    for (unsigned g = g0; g < g1; g += 8) {
-        unsigned v[8];
-#pragma unroll
-        for (int j = 0; j < 8; j++) v[j] = g + j < g1 ? gsum[(size_t)(g + j) * 256 + d] : 0u;
-#pragma unroll
-        for (int j = 0; j < 8; j++) sum += v[j];
-    }
-    s_part[q][d] = sum;
+    __threadfence();
     __syncthreads();
-    unsigned run = 0;
-    for (unsigned k = 0; k < q; k++) run += s_part[k][d];
-    for (unsigned g = g0; g < g1; g += 8) {
+    if (threadIdx.x == 0) s_last = atomicAdd(&st->ctr[slot], 1u) == ng - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // scan B: exclusive prefix over the groups per digit, the digit totals in row totals_row
+    unsigned acc = 0;
+    for (unsigned g = 0; g < ng; g += 8) {
         unsigned v[8];
 #pragma unroll
-        for (int j = 0; j < 8; j++) v[j] = g + j < g1 ? gsum[(size_t)(g + j) * 256 + d] : 0u;
+        for (int j = 0; j < 8; j++) v[j] = g + j < ng ? __ldcg(gsum + (size_t)(g + j) * 256 + d) : 0u;
 #pragma unroll
         for (int j = 0; j < 8; j++)
-            if (g + j < g1) {
-                gsum[(size_t)(g + j) * 256 + d] = run;
-                run += v[j];
+            if (g + j < ng) {
+                gsum[(size_t)(g + j) * 256 + d] = acc;
+                acc += v[j];
             }
     }
-    if (q == 3) gsum[(size_t)totals_row * 256 + d] = run;  // digit total
+    gsum[(size_t)totals_row * 256 + d] = acc;
 }
 
 template <typename KT, int ITEMS, int NB>
@@ -1070,8 +1058,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
 #undef UNIMGS_TC
                 launches++;
             }
-            k_rts_scan_a<<<ngroup_max, 256, 0, s>>>(b.tcnt, b.gsum, &b.st->K, b.st);
-            k_rts_scan_b<<<1, 1024, 0, s>>>(b.gsum, &b.st->K, ngroup_max, b.st);
+            k_rts_scan<<<ngroup_max, 256, 0, s>>>(b.tcnt, b.gsum, &b.st->K, ngroup_max, SLOT_RTS0 + pass, b.st);
             const size_t smem = onesweep_smem<uint16_t, kSortItems>();
 #define UNIMGS_DS(NB)                                                                                          \
     k_downsweep<uint16_t, kSortItems, NB><<<g2, kSortThreads, smem, s>>>(kin, b.tv[tc], (uint16_t *)b.tk[tc ^ 1], \
@@ -1080,7 +1067,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
             UNIMGS_NB_SWITCH(UNIMGS_DS)
 #undef UNIMGS_DS
 #undef UNIMGS_NB_SWITCH
-            launches += 3;
+            launches += 2;
             sh += nb;
             tc ^= 1;
         }
