@@ -42,7 +42,7 @@ class CCamera(C.Structure):
 class CSettings(C.Structure):
     _fields_ = [("alpha_max", C.c_float), ("t_eps", C.c_float), ("dilation", C.c_float),
                 ("bg", C.c_float * 3), ("bg_alpha", C.c_float), ("blend_mode", C.c_int32), ("msaa", C.c_int32),
-                ("tri_depth", C.c_int32)]
+                ("tri_depth", C.c_int32), ("resort_window", C.c_int32)]
 
 
 # blend modes: the paper's ablation (Fig.3 / Fig.4)
@@ -51,11 +51,12 @@ EXACT, NAIVE, MSAA_PIXEL, WHOLE_PIXEL, PAPER_LITERAL = range(5)
 
 class CFrag(C.Structure):
     _fields_ = [("id", C.c_uint32), ("kind", C.c_int32), ("mask", C.c_uint32), ("q", C.c_float),
-                ("depth", C.c_float), ("alpha", C.c_double), ("rgb", C.c_double * 3)]
+                ("depth", C.c_float), ("pdepth", C.c_float), ("alpha", C.c_double), ("rgb", C.c_double * 3)]
 
 
 FRAG_DTYPE = np.dtype([("id", np.uint32), ("kind", np.int32), ("mask", np.uint32), ("q", np.float32),
-                       ("depth", np.float32), ("alpha", np.float64), ("rgb", np.float64, (3,))], align=True)
+                       ("depth", np.float32), ("pdepth", np.float32), ("alpha", np.float64), ("rgb", np.float64, (3,))],
+                      align=True)
 assert FRAG_DTYPE.itemsize == C.sizeof(CFrag)
 
 _lib = None
@@ -107,6 +108,8 @@ def lib():
         L.or_rodrigues_public.restype = None
         L.or_tri_tile_depth.argtypes = [vp, i64, i32, i32]
         L.or_tri_tile_depth.restype = C.c_float
+        L.or_tri_pixel_depth.argtypes = [vp, i64, i32, i32]
+        L.or_tri_pixel_depth.restype = C.c_float
         L.or_ray_cast.argtypes = [vp, vp, i64, vp, i64, vp, vp, vp, vp]
         L.or_ray_cast.restype = i64
         L.or_bind_targets.argtypes = [vp, vp, vp, i32, C.c_float, vp]
@@ -122,11 +125,12 @@ def _ptr(a: Optional[np.ndarray]):
 
 
 def make_settings(alpha_max=0.99, t_eps=1e-4, dilation=0.3, bg=(0.0, 0.0, 0.0), bg_alpha=1.0, blend_mode=EXACT,
-                  msaa=4, tri_depth=0) -> CSettings:
-    """tri_depth: 0 = centroid sort depth (R9), 1 = plane depth at the tile centre (N8)."""
+                  msaa=4, tri_depth=0, resort_window=4) -> CSettings:
+    """tri_depth: 0 = centroid sort depth (R9), 1 = plane depth at the tile centre (N8), 2 = N8 keys and a
+    per-pixel resort window of resort_window fragments over the depth at the pixel (N9)."""
     s = CSettings()
     s.alpha_max, s.t_eps, s.dilation, s.bg_alpha = alpha_max, t_eps, dilation, bg_alpha
-    s.blend_mode, s.msaa, s.tri_depth = blend_mode, msaa, tri_depth
+    s.blend_mode, s.msaa, s.tri_depth, s.resort_window = blend_mode, msaa, tri_depth, resort_window
     for i in range(3):
         s.bg[i] = float(bg[i])
     return s
@@ -239,6 +243,10 @@ class Oracle:
     def tri_tile_depth(self, f: int, tx: int, ty: int) -> np.float32:
         """N8: sort depth of triangle f in tile (tx, ty) (after project())."""
         return np.float32(lib().or_tri_tile_depth(self._h, int(f), int(tx), int(ty)))
+
+    def tri_pixel_depth(self, f: int, x: int, y: int) -> np.float32:
+        """N9: triangle f's plane depth at the centre of pixel (x, y), clamped (after project())."""
+        return np.float32(lib().or_tri_pixel_depth(self._h, int(f), int(x), int(y)))
 
     def bins(self):
         keys = np.zeros(self.K, np.uint64)

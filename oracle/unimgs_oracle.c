@@ -53,7 +53,9 @@ typedef struct {
     float bg_alpha;
     int32_t blend_mode; /* OR_EXACT .. OR_PAPER_LITERAL */
     int32_t msaa;       /* M in {1, 2, 4, 8, 16} (P:330 uses 4) */
-    int32_t tri_depth;  /* triangle sort depth: 0 = centroid (R9), 1 = plane depth at the tile centre (N8, NEXT 3) */
+    int32_t tri_depth;  /* triangle sort depth: 0 = centroid (R9), 1 = plane depth at the tile centre (N8, NEXT 3),
+                           2 = N8 keys + a per-pixel resort window over the pixel-centre plane depth (N9) */
+    int32_t resort_window; /* tri_depth 2: window size W (<= 0: 4) */
 } or_settings;
 
 typedef struct {
@@ -61,7 +63,8 @@ typedef struct {
     int32_t kind;     /* 0 = Gaussian, 1 = triangle */
     uint32_t mask;    /* triangle coverage bits o^j, j = 0..3 */
     float q;          /* Gaussian: N6 Mahalanobis^2 */
-    float depth;
+    float depth;      /* sort (key) depth: the order of the pixel's tile list */
+    float pdepth;     /* depth at the pixel (tri_depth 2): Gaussian view z; triangle N9 */
     double alpha;
     double rgb[3];
 } or_frag;
@@ -411,7 +414,31 @@ float or_tri_tile_depth(const or_ctx *c, int64_t f, int tx, int ty) {
 
 /* sort depth of triangle f for the tile holding (tx, ty) (R9 or N8) */
 static float tri_key_depth(const or_ctx *c, int64_t f, int tx, int ty) {
-    return c->set.tri_depth == 1 ? or_tri_tile_depth(c, f, tx, ty) : c->t_depth[f];
+    return c->set.tri_depth >= 1 ? or_tri_tile_depth(c, f, tx, ty) : c->t_depth[f];
+}
+
+/* N9 (tri_depth 2; "plane-interpolated depth at the pixel centre"):
+ * N8's formula at the pixel centre P = (256 x + 128, 256 y + 128) instead of the tile
+ * centre -- w_k = E_k(P) / z_k, s = (w_0 + w_1) + w_2 in double, z = (float)(A2 / s)
+ * clamped to [min z_k, max z_k], s <= 0 gives max z_k.                              */
+float or_tri_point_depth(const or_ctx *c, int64_t f, int64_t PX, int64_t PY) {
+    const int32_t *xy = c->t_xy + 6 * f;
+    const float *z = c->t_z + 3 * f;
+    int64_t E[3];
+    for (int k = 0; k < 3; k++) {
+        const int a = (k + 1) % 3, b = (k + 2) % 3;
+        const int64_t Xa = xy[2 * a], Ya = xy[2 * a + 1], Xb = xy[2 * b], Yb = xy[2 * b + 1];
+        E[k] = (Xb - Xa) * (PY - Ya) - (Yb - Ya) * (PX - Xa);
+    }
+    const int64_t A2 = (int64_t)(xy[2] - xy[0]) * (xy[5] - xy[1]) - (int64_t)(xy[4] - xy[0]) * (xy[3] - xy[1]);
+    const double s = ((double)E[0] / (double)z[0] + (double)E[1] / (double)z[1]) + (double)E[2] / (double)z[2];
+    const float zmin = fminf(fminf(z[0], z[1]), z[2]), zmax = fmaxf(fmaxf(z[0], z[1]), z[2]);
+    if (!(s > 0.0)) return zmax;
+    return fminf(fmaxf((float)((double)A2 / s), zmin), zmax);
+}
+
+float or_tri_pixel_depth(const or_ctx *c, int64_t f, int x, int y) {
+    return or_tri_point_depth(c, f, 256 * (int64_t)x + 128, 256 * (int64_t)y + 128);
 }
 
 static float prim_depth(const or_ctx *c, uint32_t id) {
@@ -509,6 +536,7 @@ static int gaussian_fragment(const or_ctx *c, int64_t g, int x, int y, or_frag *
     fr->mask = 0;
     fr->q = q;
     fr->depth = rec[7];
+    fr->pdepth = rec[7];
     fr->alpha = a;
     for (int k = 0; k < 3; k++) fr->rgb[k] = c->g_rgb[3 * g + k];
     return 1;
@@ -624,6 +652,7 @@ static int triangle_fragment(const or_ctx *c, int64_t f, int x, int y, or_frag *
     fr->mask = m;
     fr->q = 0.0f;
     fr->depth = tri_key_depth(c, f, x / OR_TILE, y / OR_TILE);
+    fr->pdepth = c->set.tri_depth == 2 ? or_tri_pixel_depth(c, f, x, y) : fr->depth;
     fr->alpha = (double)c->topac[f];
     triangle_colour(c, f, x, y, fr->rgb);
     return 1;
@@ -737,19 +766,101 @@ int or_blend_fragments(const or_frag *fr, int n, const or_settings *set, double 
     return used;
 }
 
+/* tri_depth 2: the per-pixel resort window.  The pixel's fragments arrive in tile-list
+ * order (keys of N8); each is pushed into a window of W entries; when the window is
+ * full the entry with the smallest (bits(pdepth), id) -- incoming one included -- is
+ * blended; at the end of the list the rest are blended in that order.  A bounded
+ * priority queue: it sorts the fragments by their depth at the pixel exactly whenever
+ * none is displaced by W or more positions from its place (always, if W >= the number
+ * of the pixel's fragments).  Blending stops at termination (R16) as usual.          */
+#define OR_WMAX 64
+typedef struct {
+    or_frag w[OR_WMAX];
+    int n, cap;
+} or_window;
+
+static int frag_pless(const or_frag *a, const or_frag *b) {
+    const uint32_t da = f32_bits(a->pdepth), db = f32_bits(b->pdepth);
+    return da != db ? da < db : a->id < b->id;
+}
+
+static int win_cap(const or_settings *set) {
+    const int w = set->resort_window > 0 ? set->resort_window : 4;
+    return w > OR_WMAX ? OR_WMAX : w;
+}
+
+/* push fr; if the window overflows, write the fragment to blend into *out and return 1 */
+static int win_push(or_window *win, const or_frag *fr, or_frag *out) {
+    if (win->n < win->cap) {
+        win->w[win->n++] = *fr;
+        return 0;
+    }
+    int m = -1;
+    for (int i = 0; i < win->n; i++)
+        if (m < 0 || frag_pless(&win->w[i], &win->w[m])) m = i;
+    if (frag_pless(fr, &win->w[m])) {
+        *out = *fr;
+    } else {
+        *out = win->w[m];
+        win->w[m] = *fr;
+    }
+    return 1;
+}
+
+/* pop the smallest remaining entry; 0 when empty */
+static int win_pop(or_window *win, or_frag *out) {
+    if (!win->n) return 0;
+    int m = 0;
+    for (int i = 1; i < win->n; i++)
+        if (frag_pless(&win->w[i], &win->w[m])) m = i;
+    *out = win->w[m];
+    win->w[m] = win->w[--win->n];
+    return 1;
+}
+
+/* Blend one fragment of the pixel's list order, through the window for tri_depth 2. */
+static void pix_feed(or_pix *s, or_window *win, const or_frag *fr, const or_settings *set, uint32_t *cnt) {
+    or_frag e;
+    const or_frag *apply = fr;
+    if (set->tri_depth == 2) {
+        if (!win_push(win, fr, &e)) return;
+        apply = &e;
+    }
+    pix_apply(s, apply, set);
+    if (cnt) {
+        cnt[apply->kind == 0 ? 0 : 1]++;
+        cnt[2] = apply->id;
+    }
+}
+
+static void pix_drain(or_pix *s, or_window *win, const or_settings *set, uint32_t *cnt) {
+    or_frag e;
+    while (set->tri_depth == 2 && !s->done && win_pop(win, &e)) {
+        pix_apply(s, &e, set);
+        if (cnt) {
+            cnt[e.kind == 0 ? 0 : 1]++;
+            cnt[2] = e.id;
+        }
+    }
+}
+
 /* Tiled render: per pixel, walk its tile's sorted list (keys, ranges from or_bin). */
 static void render_pixel_tiled(const or_ctx *c, int x, int y, double out[4]) {
     int tile = (y / OR_TILE) * c->tiles_x + (x / OR_TILE);
     uint32_t b = c->ranges[2 * tile], e = c->ranges[2 * tile + 1];
     or_pix s;
     pix_init(&s, &c->set);
+    or_window win;
+    win.n = 0;
+    win.cap = win_cap(&c->set);
     or_frag fr;
     for (uint32_t i = b; i < e && !s.done; i++) {
         uint32_t p = c->vals[i];
         int hit = (int64_t)p < c->F ? triangle_fragment(c, p, x, y, &fr)
                                     : gaussian_fragment(c, (int64_t)p - c->F, x, y, &fr);
-        if (hit) pix_apply(&s, &fr, &c->set);
+        if (hit) pix_feed(&s, &win, &fr, &c->set, NULL);
     }
+    pix_drain(&s, &win, &c->set, NULL);
     pix_finish(&s, &c->set, out);
 }
 
@@ -763,6 +874,9 @@ static void count_pixel_tiled(const or_ctx *c, int x, int y, uint32_t out[4]) {
     uint32_t b = c->ranges[2 * tile], e = c->ranges[2 * tile + 1];
     or_pix s;
     pix_init(&s, &c->set);
+    or_window win;
+    win.n = 0;
+    win.cap = win_cap(&c->set);
     or_frag fr;
     out[0] = out[1] = out[3] = 0;
     out[2] = 0xFFFFFFFFu;
@@ -770,11 +884,9 @@ static void count_pixel_tiled(const or_ctx *c, int x, int y, uint32_t out[4]) {
         uint32_t p = c->vals[i];
         int hit = (int64_t)p < c->F ? triangle_fragment(c, p, x, y, &fr)
                                     : gaussian_fragment(c, (int64_t)p - c->F, x, y, &fr);
-        if (!hit) continue;
-        pix_apply(&s, &fr, &c->set);
-        out[fr.kind == 0 ? 0 : 1]++;
-        out[2] = p;
+        if (hit) pix_feed(&s, &win, &fr, &c->set, out);
     }
+    pix_drain(&s, &win, &c->set, out);
 }
 
 int or_render_counts(const or_ctx *c, uint32_t *out, const int32_t *tiles, int64_t n_tiles, int nthreads) {
@@ -891,7 +1003,11 @@ int or_render_bruteforce(or_ctx *c, double *out, int nthreads) {
                 double *o = out + 4 * ((int64_t)y * W + x);
                 or_pix s;
                 pix_init(&s, &c->set);
-                for (int64_t i = 0; i < n && !s.done; i++) pix_apply(&s, buf + i, &c->set);
+                or_window win;
+                win.n = 0;
+                win.cap = win_cap(&c->set);
+                for (int64_t i = 0; i < n && !s.done; i++) pix_feed(&s, &win, buf + i, &c->set, NULL);
+                pix_drain(&s, &win, &c->set, NULL);
                 pix_finish(&s, &c->set, o);
             }
         free(buf);
@@ -931,7 +1047,9 @@ int or_render_supersampled(or_ctx *c, double *out, int S, int nthreads) {
                         for (int64_t f = 0; f < c->F; f++) {
                             if (!c->t_touched[f] || !or_inside(c->t_xy + 6 * f, PX, PY)) continue;
                             buf[n].id = (uint32_t)f; buf[n].kind = 1; buf[n].mask = 1;
-                            buf[n].depth = tri_key_depth(c, f, x / OR_TILE, y / OR_TILE);
+                            /* tri_depth 2: the truth orders by the plane depth at the sub-sample */
+                            buf[n].depth = c->set.tri_depth == 2 ? or_tri_point_depth(c, f, PX, PY)
+                                                                 : tri_key_depth(c, f, x / OR_TILE, y / OR_TILE);
                             buf[n].alpha = (double)c->topac[f];
                             triangle_colour_at(c, f, PX, PY, buf[n].rgb);
                             n++;
