@@ -153,6 +153,14 @@ typedef struct {
  *       clamped to the triangle's z range (N8) -- interpenetrating
  *       surfaces swap order across tiles.  Per-pair keys need the full 64-bit
  *       sort, so tri_depth 1 always bins as sort_mode 1.
+ *   2 = the keys of 1, plus a per-pixel resort window in the blend (SPEC S:235:
+ *       triangle fragments ordered by their plane depth at the pixel centre):
+ *       each pixel passes its fragments, in list order, through a bounded
+ *       priority queue of 4 entries on (bits(depth at the pixel), id) -- the
+ *       plane depth at the pixel centre clamped to the triangle's z range (N9)
+ *       for a triangle, the view z for a Gaussian -- blending the smallest on
+ *       overflow and the rest at the end of the list, so surfaces swap order
+ *       at the pixel where they cross.  blend_mode 0 and msaa_samples 4 only.
  * sort_ctas_per_sm: persistent CTAs per SM of the radix-sort passes, 1..4, or
  *   0 = automatic (4 for a context rendering alone; 1 for the contexts of a
  *   unimgs_render_host call with several lanes).  4 gives the lowest latency

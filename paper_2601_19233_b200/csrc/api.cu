@@ -136,7 +136,9 @@ static int validate_settings(unimgs_ctx *c, const unimgs_settings *s) {
     if (!(s->t_eps >= 0.f && s->t_eps < 1.f)) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "t_eps not in [0,1)");
     if (!(s->dilation >= 0.f && std::isfinite(s->dilation))) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "dilation < 0");
     if (s->sort_mode != 0 && s->sort_mode != 1) return fail(c, UNIMGS_ERR_UNSUPPORTED, "sort_mode must be 0 or 1");
-    if (s->tri_depth != 0 && s->tri_depth != 1) return fail(c, UNIMGS_ERR_UNSUPPORTED, "tri_depth must be 0 or 1");
+    if (s->tri_depth < 0 || s->tri_depth > 2) return fail(c, UNIMGS_ERR_UNSUPPORTED, "tri_depth must be 0, 1 or 2");
+    if (s->tri_depth == 2 && (s->blend_mode != 0 || s->msaa_samples != 4))
+        return fail(c, UNIMGS_ERR_UNSUPPORTED, "tri_depth 2 (per-pixel resort) needs blend_mode 0 and msaa_samples 4");
     if (s->sort_ctas_per_sm < 0 || s->sort_ctas_per_sm > 4)
         return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "sort_ctas_per_sm must be 0..4");
     for (int i = 0; i < 3; i++)
@@ -356,7 +358,7 @@ extern "C" int unimgs_render(unimgs_ctx *c, float *out, void *stream) {
     if (c->stage < 2) return fail(c, UNIMGS_ERR_STATE, "render before bin");
     if (!out) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "out is NULL");
     BlendParams bp{c->set.alpha_max, c->set.t_eps, c->set.bg_alpha, {c->set.bg[0], c->set.bg[1], c->set.bg[2]},
-                   c->set.blend_mode, c->set.msaa_samples};
+                   c->set.blend_mode, c->set.msaa_samples, c->set.tri_depth == 2};
     c->launches += launch_blend(c->buf, c->g, c->m, c->cam, bp, out, (cudaStream_t)stream);
     return check_launch(c, "render");
 }
@@ -368,7 +370,7 @@ extern "C" int unimgs_render_counted(unimgs_ctx *c, float *out, int64_t *work_ho
     cudaStream_t s = (cudaStream_t)stream;
     CUDA_TRY(c, cudaMemsetAsync(c->buf.st->work, 0, sizeof(c->buf.st->work), s));
     BlendParams bp{c->set.alpha_max, c->set.t_eps, c->set.bg_alpha, {c->set.bg[0], c->set.bg[1], c->set.bg[2]},
-                   c->set.blend_mode, c->set.msaa_samples};
+                   c->set.blend_mode, c->set.msaa_samples, c->set.tri_depth == 2};
     c->launches += launch_blend(c->buf, c->g, c->m, c->cam, bp, out, s, true);
     int rc = check_launch(c, "render_counted");
     if (rc) return rc;
@@ -385,7 +387,7 @@ extern "C" int unimgs_render_fragments(unimgs_ctx *c, float *out, uint32_t *coun
     if (!out || !counts) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "out/counts is NULL");
     cudaStream_t s = (cudaStream_t)stream;
     BlendParams bp{c->set.alpha_max, c->set.t_eps, c->set.bg_alpha, {c->set.bg[0], c->set.bg[1], c->set.bg[2]},
-                   c->set.blend_mode, c->set.msaa_samples};
+                   c->set.blend_mode, c->set.msaa_samples, c->set.tri_depth == 2};
     c->launches += launch_blend(c->buf, c->g, c->m, c->cam, bp, out, s, true, counts);
     return check_launch(c, "render_fragments");
 }

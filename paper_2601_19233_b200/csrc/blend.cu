@@ -600,6 +600,317 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
     }
 }
 
+// ----------------------------------------------------------------------------
+// tri_depth 2: the per-pixel resort window (SPEC S:235/S:280:
+// triangle fragments ordered by their plane depth at the pixel centre).  The tile
+// lists are keyed like tri_depth 1 (N8); every pixel passes its fragments, in list
+// order, through a window of kResortW entries in shared memory -- a bounded priority
+// queue on (bits(depth at the pixel), id): N9 (N8's plane depth at the pixel centre,
+// IEEE double as in the oracle) for a triangle, the view z for a Gaussian -- and
+// blends the smallest entry whenever the window overflows, the rest at the end of
+// the list (the oracle's or_window).  Exact-entity mode, M = 4 only; a quality
+// variant, not the throughput path.
+// ----------------------------------------------------------------------------
+constexpr int kResortW = 4;
+
+struct WinE {
+    float a, r, g, b;
+    unsigned mk;    // triangle: coverage mask | 1 << 31; Gaussian: 0
+    unsigned dbits; // bits(depth at the pixel)
+    unsigned id;
+    unsigned pad;
+};
+
+__device__ __forceinline__ bool win_less(unsigned da, unsigned ia, unsigned db, unsigned ib) {
+    return da != db ? da < db : ia < ib;
+}
+
+// N9: triangle plane depth at the pixel centre from the exact centre edge functions
+__device__ __forceinline__ unsigned pixel_plane_depth_bits(const int X[3], const int Y[3], const long long Ec[3],
+                                                           const TriAttr &r) {
+    const long long A2 = (long long)(X[1] - X[0]) * (Y[2] - Y[0]) - (long long)(X[2] - X[0]) * (Y[1] - Y[0]);
+    const double sd = __dadd_rn(__dadd_rn(__ddiv_rn((double)Ec[0], (double)r.q2.x), __ddiv_rn((double)Ec[1], (double)r.q2.y)),
+                                __ddiv_rn((double)Ec[2], (double)r.q2.z));
+    const float zmin = fminf(fminf(r.q2.x, r.q2.y), r.q2.z), zmax = fmaxf(fmaxf(r.q2.x, r.q2.y), r.q2.z);
+    if (!(sd > 0.0)) return __float_as_uint(zmax);
+    return __float_as_uint(fminf(fmaxf(__double2float_rn(__ddiv_rn((double)A2, sd)), zmin), zmax));
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(kBlendThreads, 3) k_blend_resort(const uint2 *__restrict__ ranges,
+                                                                 const uint32_t *__restrict__ order,
+                                                                 const uint32_t *__restrict__ vals,
+                                                                 const GaussRecord *__restrict__ grec,
+                                                                 const TriRecord *__restrict__ trec,
+                                                                 const uint32_t *__restrict__ dkey, TexView tv,
+                                                                 unsigned F, int W, int H, int tiles_x, BlendParams bp,
+                                                                 float4 *__restrict__ out, DevState *st,
+                                                                 uint4 *__restrict__ frag_counts) {
+    constexpr int M = 4, MODE = MODE_EXACT;
+    if (st->overflow) return;
+    constexpr int NW = kBlendThreads / 32;
+    unsigned long long w_gt = 0, w_gf = 0, w_tt = 0, w_tf = 0;
+    unsigned last_id = 0xFFFFFFFFu;
+    __shared__ unsigned s_ids[NW][32];
+    __shared__ float s_dep[NW][32];  // a packed Gaussian's view z
+    __shared__ WarpBuf s_buf[NW];
+    __shared__ float4 s_stage[NW][32][3];
+    __shared__ TriAttr s_tri[NW][32];
+    extern __shared__ __align__(16) WinE s_win[];  // [kResortW][kBlendThreads]
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile = (int)__ldg(order + blockIdx.x);
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int sx0 = tx * kTile + (warp & 1) * 8, sy0 = ty * kTile + (warp >> 1) * 4;
+    const int x = sx0 + (lane & 7), y = sy0 + (lane >> 3);
+    const float px = (float)x + 0.5f;
+    const uint2 rg = ranges[tile];
+    const unsigned lt = (1u << lane) - 1u;
+    WarpBuf &wb = s_buf[warp];
+    float *ef = &wb.e[0][0].x;
+    TriAttr *tat = s_tri[warp];
+    float4 *stg = s_stage[warp][lane];
+    const unsigned stg_s = (unsigned)__cvta_generic_to_shared(stg);
+    WinE *win = s_win + threadIdx.x;  // entry j at win[j * kBlendThreads]
+    int wn = 0;
+
+    Px<MODE, M> s;
+    s.C0 = s.C1 = s.C2 = 0.f;
+    s.T = s.Te = s.G = s.Tl = 1.f;
+#pragma unroll
+    for (int j = 0; j < M; j++) s.t[j] = 1.f;
+    s.open = false;
+    s.Tlast = __int_as_float(0x7fc00000);
+    s.py = (float)y + 0.5f;
+    if (!(x < W && y < H)) s.finish();
+
+    auto apply = [&](const WinE &e) {  // the state machine, one fragment
+        if (COUNT) {
+            if (e.mk >> 31) w_tf++;
+            else w_gf++;
+            last_id = e.id;
+        }
+        if (!(e.mk >> 31)) {  // Gaussian: Eq.1-2 (T holds an open entity's exit T, R3)
+            const float w = s.T * e.a;
+            s.C0 += w * e.r; s.C1 += w * e.g; s.C2 += w * e.b;
+            s.T -= w;
+        } else {  // triangle: Eq.7-9 in a depth-adjacent entity
+            const unsigned m = e.mk & 0xFu;
+            if (!(s.T == s.Tlast)) {
+                s.Te = s.T;
+#pragma unroll
+                for (int j = 0; j < M; j++) s.t[j] = 1.f;
+            }
+            float O = 0.f;
+#pragma unroll
+            for (int j = 0; j < M; j++) O += ((m >> j) & 1u) ? s.t[j] : 0.f;
+            O *= 1.f / M;
+            const float w = s.Te * O * e.a;
+            s.C0 += w * e.r; s.C1 += w * e.g; s.C2 += w * e.b;
+            const float kk = 1.f - e.a;
+#pragma unroll
+            for (int j = 0; j < M; j++)
+                if ((m >> j) & 1u) s.t[j] *= kk;
+            s.T = s.exit_T();
+            s.Tlast = s.T;
+        }
+        if (s.T < bp.t_eps) s.finish();
+    };
+    auto push = [&](const WinE &e) {  // into the window; blends the smallest on overflow
+        if (wn < kResortW) {
+            win[wn * kBlendThreads] = e;
+            wn++;
+            return;
+        }
+        int mi = 0;
+        WinE best = win[0];
+        for (int j = 1; j < kResortW; j++) {
+            const WinE c = win[j * kBlendThreads];
+            if (win_less(c.dbits, c.id, best.dbits, best.id)) { best = c; mi = j; }
+        }
+        if (win_less(e.dbits, e.id, best.dbits, best.id)) {
+            apply(e);
+        } else {
+            apply(best);
+            win[mi * kBlendThreads] = e;
+        }
+    };
+
+    auto stage_rec = [&](unsigned id) {
+        if (id != 0xFFFFFFFFu) {
+            const char *src = id >= F ? reinterpret_cast<const char *>(grec + (id - F))
+                                      : reinterpret_cast<const char *>(trec + id);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(stg_s), "l"(src) : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(stg_s + 16), "l"(src + 16) : "memory");
+            if (id >= F)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(stg_s + 32), "l"(src + 32) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    unsigned id0 = rg.x + lane < rg.y ? __ldg(vals + rg.x + lane) : 0xFFFFFFFFu;
+    unsigned id1 = rg.x + 32 + lane < rg.y ? __ldg(vals + rg.x + 32 + lane) : 0xFFFFFFFFu;
+    stage_rec(id0);
+    const float kexp = -0.72134752044448170f;
+
+    for (unsigned base = rg.x; base < rg.y; base += 32) {
+        const unsigned live = __ballot_sync(0xffffffffu, !s.done());
+        if (!live) break;
+        LiveBox lb;
+        {
+            const unsigned cols = (live | (live >> 8) | (live >> 16) | (live >> 24)) & 0xFFu;
+            const int c0 = __ffs(cols) - 1, c1 = 31 - __clz(cols);
+            const int r0 = (__ffs(live) - 1) >> 3, r1 = (31 - __clz(live)) >> 3;
+            lb.cx0 = (float)(sx0 + c0) + 0.5f; lb.cx1 = (float)(sx0 + c1) + 0.5f;
+            lb.cy0 = (float)(sy0 + r0) + 0.5f; lb.cy1 = (float)(sy0 + r1) + 0.5f;
+            lb.X0 = 256 * (sx0 + c0); lb.X1 = 256 * (sx0 + c1 + 1) - 1;
+            lb.Y0 = 256 * (sy0 + r0); lb.Y1 = 256 * (sy0 + r1 + 1) - 1;
+        }
+        const unsigned id = id0;
+        id0 = id1;
+        id1 = base + 64 + lane < rg.y ? __ldg(vals + base + 64 + lane) : 0xFFFFFFFFu;
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        bool rel = false;
+        float4 a, b, c;
+        if (id != 0xFFFFFFFFu) {
+            a = stg[0];
+            b = stg[1];
+            if (id >= F) {
+                c = stg[2];
+                rel = gauss_touches(a, b, c, lb);
+            } else {
+                rel = tri_touches(a, b, lb);
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, rel);
+        const unsigned cnt = __popc(bal);
+        const unsigned slot = __popc(bal & lt);
+        if (rel) {
+            s_ids[warp][slot] = id;
+            float *e = ef + 12 * (slot >> 1) + (slot & 1);
+            if (id >= F) {
+                e[0] = a.x; e[2] = a.y; e[4] = b.x; e[6] = b.z; e[8] = b.y + b.y; e[10] = a.z;
+                wb.col[slot] = make_float4(c.x, c.y, c.z, lg2_ftz(a.w));
+                s_dep[warp][slot] = __uint_as_float(__ldg(dkey + id));
+            } else {
+                e[0] = a.x; e[2] = a.y; e[4] = a.z; e[6] = a.w; e[8] = b.x; e[10] = -1.f;
+                wb.col[slot] = make_float4(b.y, b.z, b.w, __uint_as_float(id));
+                const char *src = reinterpret_cast<const char *>(&trec[id].q2);
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(&tat[slot]);
+#pragma unroll
+                for (int w = 0; w < 4; w++)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * w), "l"(src + 16 * w)
+                                 : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        __syncwarp();
+        stage_rec(id0);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        __syncwarp();
+        for (unsigned p = 0; 2 * p < cnt; p++) {
+            float q[2], m[2];
+            {
+                const float4 A = wb.e[p][0], B = wb.e[p][1], Cc = wb.e[p][2];
+                const f32x2 dx = sub2(pk2(px, px), pk2(A.x, A.y));
+                const f32x2 dy = sub2(pk2(s.py, s.py), pk2(A.z, A.w));
+                const f32x2 t = fma2(pk2(B.z, B.w), mul2(dy, dy), mul2(pk2(Cc.x, Cc.y), mul2(dx, dy)));
+                upk2(fma2(pk2(B.x, B.y), mul2(dx, dx), t), q[0], q[1]);
+                m[0] = Cc.z;
+                m[1] = Cc.w;
+            }
+#pragma unroll
+            for (int j = 0; j < 2; j++) {
+                const unsigned k = 2 * p + j;
+                if (k >= cnt) break;
+                if (m[j] >= 0.f) {  // Gaussian entry
+                    if (COUNT && !s.done()) w_gt++;
+                    if (q[j] <= m[j] && !s.done()) {
+                        const float4 ec = wb.col[k];
+                        WinE e;
+                        e.a = fminf(bp.alpha_max, ex2_ftz(fmaf(q[j], kexp, ec.w)));
+                        e.r = ec.x; e.g = ec.y; e.b = ec.z;
+                        e.mk = 0;
+                        e.dbits = __float_as_uint(s_dep[warp][k]);
+                        e.id = s_ids[warp][k];
+                        push(e);
+                    }
+                    continue;
+                }
+                if (s.done()) continue;
+                const float *e = ef + 12 * p + j;
+                const float4 ec = wb.col[k];
+                const int X[3] = {__float_as_int(e[0]), __float_as_int(e[4]), __float_as_int(e[8])};
+                const int Y[3] = {__float_as_int(e[2]), __float_as_int(e[6]), __float_as_int(ec.x)};
+                if (COUNT) w_tt++;
+                {   // exact pre-test: no sample can lie in the triangle's bbox
+                    constexpr int R16 = 16 * 6;
+                    const int PX = 256 * x + 128, PY = 256 * y + 128;
+                    if (PX + R16 < min(X[0], min(X[1], X[2])) || PX - R16 > max(X[0], max(X[1], X[2])) ||
+                        PY + R16 < min(Y[0], min(Y[1], Y[2])) || PY - R16 > max(Y[0], max(Y[1], Y[2])))
+                        continue;
+                }
+                long long Ec[3];
+                const unsigned mk = coverage<M>(X, Y, x, y, Ec);
+                if (!mk) continue;
+                float rgb[3];
+                tri_colour(tat[k], __float_as_int(ec.y), Ec, tv, rgb);
+                WinE we;
+                we.a = ec.z;
+                we.r = rgb[0]; we.g = rgb[1]; we.b = rgb[2];
+                we.mk = mk | 0x80000000u;
+                we.dbits = pixel_plane_depth_bits(X, Y, Ec, tat[k]);
+                we.id = __float_as_uint(ec.w);
+                push(we);
+            }
+        }
+        __syncwarp();
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    // end of the list: blend the window's rest in (depth, id) order
+    while (wn > 0 && !s.done()) {
+        int mi = 0;
+        WinE best = win[0];
+        for (int j = 1; j < wn; j++) {
+            const WinE c2 = win[j * kBlendThreads];
+            if (win_less(c2.dbits, c2.id, best.dbits, best.id)) { best = c2; mi = j; }
+        }
+        apply(best);
+        win[mi * kBlendThreads] = win[(wn - 1) * kBlendThreads];
+        wn--;
+    }
+    if (COUNT && frag_counts && x < W && y < H)
+        frag_counts[(size_t)y * W + x] = make_uint4((unsigned)w_gf, (unsigned)w_tf, last_id, (unsigned)w_gt);
+    if (COUNT) {
+        unsigned long long v[4] = {w_gt, w_gf, w_tt, w_tf};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            unsigned long long xs = v[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+            if (lane == 0 && xs) atomicAdd(&st->work[k], xs);
+        }
+    }
+    if (x < W && y < H) {
+        const float sb = s.T * bp.bg_alpha;
+        out[(size_t)y * W + x] = make_float4(s.C0 + sb * bp.bg[0], s.C1 + sb * bp.bg[1], s.C2 + sb * bp.bg[2], s.T);
+    }
+}
+
+template <bool COUNT>
+static void launch_resort(const Buffers &b, const MeshInput &m, const CamParams &cam, const BlendParams &bp, float *out,
+                          cudaStream_t s, uint32_t *fc) {
+    const size_t smem = sizeof(WinE) * kResortW * kBlendThreads;
+    static const bool attr = [smem] {
+        cudaFuncSetAttribute(k_blend_resort<COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return true;
+    }();
+    (void)attr;
+    TexView tv{reinterpret_cast<const uchar4 *>(m.tex), m.tw, m.th};
+    k_blend_resort<COUNT><<<cam.tiles_x * cam.tiles_y, kBlendThreads, smem, s>>>(
+        b.ranges, b.order, b.sorted_vals, b.grec, b.trec, b.dkey, tv, (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
+        reinterpret_cast<float4 *>(out), b.st, reinterpret_cast<uint4 *>(fc));
+}
+
 template <int MODE, int M>
 static void launch_mode(const Buffers &b, const MeshInput &m, const CamParams &cam, const BlendParams &bp, float *out,
                         cudaStream_t s, bool count_work, uint32_t *frag_counts) {
@@ -631,6 +942,11 @@ static void launch_m(int M, const Buffers &b, const MeshInput &m, const CamParam
 int launch_blend(const Buffers &b, const GaussInput &g, const MeshInput &m, const CamParams &cam,
                  const BlendParams &bp, float *out, cudaStream_t s, bool count_work, uint32_t *fc) {
     (void)g;
+    if (bp.resort) {  // tri_depth 2 (exact mode, M = 4: validated by the API)
+        if (count_work) launch_resort<true>(b, m, cam, bp, out, s, fc);
+        else launch_resort<false>(b, m, cam, bp, out, s, nullptr);
+        return 1;
+    }
     switch (bp.mode) {
         case MODE_NAIVE: launch_m<MODE_NAIVE>(bp.msaa, b, m, cam, bp, out, s, count_work, fc); break;
         case MODE_MSAA_PIXEL: launch_m<MODE_MSAA_PIXEL>(bp.msaa, b, m, cam, bp, out, s, count_work, fc); break;

@@ -134,6 +134,7 @@ struct BlendParams {
     float bg[3];
     int mode;   // unimgs_settings::blend_mode
     int msaa;   // M samples
+    int resort; // tri_depth 2: the per-pixel resort window (k_blend_resort)
 };
 
 struct BindInput {
