@@ -215,6 +215,15 @@ UNIMGS_API int unimgs_reserve2(unimgs_ctx *c, int64_t max_gaussians, int64_t max
 UNIMGS_API int unimgs_preprocess(unimgs_ctx *c, const unimgs_gaussians *g, const unimgs_mesh *m,
                       const unimgs_camera *cam, void *stream);
 
+/* unimgs_preprocess for n <= 4 views of ONE scene at once, view v into context
+ * ctxs[v] (distinct, reserved, equal dilation): every Gaussian's inputs and its
+ * Sigma (N3) are read / computed once for all n views, so the scene crosses HBM
+ * once per n views instead of once per view (the multi-view batch of BASELINE
+ * configs[4]).  Each context's records are bit-identical to a unimgs_preprocess
+ * of its view; each is then binned and rendered on its own (after `stream`). */
+UNIMGS_API int unimgs_preprocess_multi(unimgs_ctx *const *ctxs, int32_t n, const unimgs_gaussians *g,
+                                       const unimgs_mesh *m, const unimgs_camera *cams, void *stream);
+
 /* Duplicate (tile, primitive) pairs, sort them by (tile, depth bits, id) and
  * compute per-tile ranges.  Exactly once per unimgs_preprocess (the
  * per-frame counters it consumes are reset only by preprocess): a second bin

@@ -19,7 +19,8 @@ EXPORTS = ("unimgs_default_settings", "unimgs_create", "unimgs_set_settings", "u
            "unimgs_preprocess", "unimgs_bin", "unimgs_render", "unimgs_render_counted", "unimgs_get_stats", "unimgs_get_bins",
            "unimgs_get_records", "unimgs_render_host", "unimgs_launch_count", "unimgs_error_string",
            "unimgs_destroy", "unimgs_deform", "unimgs_bind", "unimgs_render_host_async", "unimgs_host_wait",
-           "unimgs_set_host_lanes", "unimgs_render_fragments", "unimgs_debug_check_guards")
+           "unimgs_set_host_lanes", "unimgs_render_fragments", "unimgs_debug_check_guards",
+           "unimgs_preprocess_multi")
 
 
 class BindSettings(C.Structure):
@@ -86,6 +87,7 @@ def load():
     L.unimgs_reserve2.argtypes = [vp, i64, i64, i64, i32, i32]
     L.unimgs_preprocess.argtypes = [vp, C.POINTER(Gaussians), C.POINTER(Mesh), C.POINTER(Camera), vp]
     L.unimgs_bin.argtypes = [vp, vp]
+    L.unimgs_preprocess_multi.argtypes = [vp, C.c_int32, C.POINTER(Gaussians), C.POINTER(Mesh), C.POINTER(Camera), vp]
     L.unimgs_render.argtypes = [vp, vp, vp]
     L.unimgs_render_counted.argtypes = [vp, vp, vp, vp]
     L.unimgs_render_fragments.argtypes = [vp, vp, vp, vp]
@@ -113,7 +115,8 @@ def load():
     L.unimgs_destroy.restype = None
     for name in ("unimgs_create", "unimgs_set_settings", "unimgs_reserve", "unimgs_reserve2", "unimgs_preprocess",
                  "unimgs_bin", "unimgs_render", "unimgs_render_counted", "unimgs_get_stats", "unimgs_get_bins", "unimgs_get_records",
-                 "unimgs_render_host", "unimgs_render_fragments", "unimgs_debug_check_guards"):
+                 "unimgs_render_host", "unimgs_render_fragments", "unimgs_debug_check_guards",
+                 "unimgs_preprocess_multi"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L

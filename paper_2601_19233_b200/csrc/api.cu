@@ -337,6 +337,73 @@ extern "C" int unimgs_preprocess(unimgs_ctx *c, const unimgs_gaussians *g, const
     return UNIMGS_OK;
 }
 
+extern "C" int unimgs_preprocess_multi(unimgs_ctx *const *ctxs, int32_t n, const unimgs_gaussians *g,
+                                       const unimgs_mesh *m, const unimgs_camera *cams, void *stream) {
+    if (!ctxs || !cams || n < 1) return UNIMGS_ERR_INVALID_ARGUMENT;
+    if (n > kMaxMultiViews) return fail(ctxs[0], UNIMGS_ERR_UNSUPPORTED, "preprocess_multi: at most %d views", kMaxMultiViews);
+    for (int v = 0; v < n; v++) {
+        if (!ctxs[v]) return UNIMGS_ERR_INVALID_ARGUMENT;
+        for (int u = 0; u < v; u++)
+            if (ctxs[u] == ctxs[v]) return fail(ctxs[v], UNIMGS_ERR_INVALID_ARGUMENT, "preprocess_multi: a context twice");
+    }
+    // every host check of unimgs_preprocess, per view, before anything is enqueued
+    GaussInput gi{};
+    MeshInput mi{};
+    MultiView mv{};
+    mv.n = n;
+    for (int v = 0; v < n; v++) {
+        unimgs_ctx *c = ctxs[v];
+        if (!c->reserved) return fail(c, UNIMGS_ERR_STATE, "preprocess before reserve");
+        int rc = make_cam(c, &cams[v], mv.cam[v]);
+        if (rc) return rc;
+        if (g && g->count > 0) {
+            if (g->count > c->max_g)
+                return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "gaussian count %lld above reserved %lld",
+                            (long long)g->count, (long long)c->max_g);
+            if (!g->means || (!g->cov3d && (!g->quats || !g->scales)) || !g->opacities || !g->sh)
+                return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "gaussian array is NULL");
+            if (g->sh_degree < 0 || g->sh_degree > 3) return fail(c, UNIMGS_ERR_UNSUPPORTED, "sh_degree must be 0..3");
+            gi = GaussInput{g->count, g->means, g->quats, g->scales, g->opacities, g->sh, g->sh_degree, g->cov3d};
+        } else if (g && g->count < 0) {
+            return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "negative gaussian count");
+        }
+        if (m && m->num_triangles > 0) {
+            if (m->num_triangles > c->max_t) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "triangle count above reserved");
+            if (m->num_vertices < 1 || !m->positions || !m->faces || !m->opacity)
+                return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "mesh array is NULL");
+            if (m->texture && (m->tex_width < 1 || m->tex_height < 1))
+                return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "texture size < 1");
+            const uint8_t *tex = (m->texture && m->uvs) ? m->texture : nullptr;
+            mi = MeshInput{m->num_vertices, m->num_triangles, m->positions, m->uvs, m->colors, m->opacity, m->faces,
+                           tex, m->tex_width, m->tex_height};
+        } else if (m && (m->num_triangles < 0 || m->num_vertices < 0)) {
+            return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "negative mesh count");
+        }
+        if (gi.N + mi.F > c->max_prims) return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "N + F above reserved");
+        if (c->set.dilation != ctxs[0]->set.dilation)
+            return fail(c, UNIMGS_ERR_INVALID_ARGUMENT, "preprocess_multi: the contexts' dilations differ");
+        mv.buf[v] = c->buf;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int v = 0; v < n; v++) {
+        unimgs_ctx *c = ctxs[v];
+        c->launches += launch_begin_frame(c->buf.st, s);
+        c->launches += launch_setup_triangles(mi, mv.cam[v], c->buf, s);
+    }
+    ctxs[0]->launches += launch_preprocess_gaussians_multi(gi, mi.F, mv, ctxs[0]->set.dilation, s);
+    int rc = check_launch(ctxs[0], "preprocess_multi");
+    if (rc) return rc;
+    for (int v = 0; v < n; v++) {
+        unimgs_ctx *c = ctxs[v];
+        c->g = gi;
+        c->m = mi;
+        c->cam = mv.cam[v];
+        c->P = gi.N + mi.F;
+        c->stage = 1;
+    }
+    return UNIMGS_OK;
+}
+
 extern "C" int unimgs_bin(unimgs_ctx *c, void *stream) {
     if (!c) return UNIMGS_ERR_INVALID_ARGUMENT;
     // exactly one bin per preprocess: only k_begin_frame (run by preprocess) resets the

@@ -149,11 +149,22 @@ struct BindInput {
     const int32_t *faces;                 // device [F][3]
 };
 
+// Several views of one scene for the multi-view Gaussian preprocess (each view: its
+// camera and its context's buffers).
+constexpr int kMaxMultiViews = 4;
+struct MultiView {
+    int n;
+    CamParams cam[kMaxMultiViews];
+    Buffers buf[kMaxMultiViews];
+};
+
 // ---- launchers (return number of kernels enqueued) --------------------------
 int launch_begin_frame(DevState *st, cudaStream_t s);
 int launch_preprocess_gaussians(const GaussInput &g, int64_t F, const CamParams &cam, float dilation,
                                 const Buffers &b, cudaStream_t s);
 int launch_setup_triangles(const MeshInput &m, const CamParams &cam, const Buffers &b, cudaStream_t s);
+int launch_preprocess_gaussians_multi(const GaussInput &g, int64_t F, const MultiView &mv, float dilation,
+                                      cudaStream_t s);
 // binning: factored (sort_mode 0) or full 64-bit keys (sort_mode 1)
 // Look-back rows the sort passes need (one per sort tile of the largest pass).
 int64_t sort_lookback_tiles(int64_t max_pairs, int64_t max_prims);

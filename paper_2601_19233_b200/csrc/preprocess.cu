@@ -113,16 +113,150 @@ __device__ __forceinline__ void sh_eval(const float *__restrict__ sh, int deg, f
     out[2] = fmaxf(bl + 0.5f, 0.f);
 }
 
+// The per-view part of B1 for Gaussian g (N1, N2, N4, N5, SH): writes the record,
+// rect and depth key of view `cam` into `b` and returns whether g is visible;
+// get_sig(Sig) supplies Sigma (N3, or the given cov3d) -- only called once g passed
+// the near/far cull, so the multi-view kernel can compute it once for all views.
+template <typename GetSig>
+__device__ __forceinline__ bool project_gaussian(const GaussInput &gin, int64_t g, int64_t F, const CamParams &cam,
+                                                 float dilation, const Buffers &b, float mx, float my, float mz, float o,
+                                                 uint32_t &touched, GetSig get_sig) {
+    const int64_t p = F + g;
+    bool vis = false;
+    touched = 0;
+    do {
+        float pv[3];
+        view_point(cam, mx, my, mz, pv);
+        if (!(pv[2] > cam.near_z) || pv[2] > cam.far_z) break;
+        const float xz = dv(pv[0], pv[2]), yz = dv(pv[1], pv[2]);          // N2
+        const float u = fma_(cam.fx, xz, cam.cx), v = fma_(cam.fy, yz, cam.cy);
+#if UNIMGS_SH_PREFETCH
+        // likely visible: start pulling its SH coefficients into L2 now, so the
+        // EWA math below hides the latency of the dependent SH loads
+        if (u > -(float)cam.W && u < 2.f * (float)cam.W && v > -(float)cam.H && v < 2.f * (float)cam.H) {
+            const char *shp = reinterpret_cast<const char *>(gin.sh + g * (gin.sh_degree + 1) * (gin.sh_degree + 1) * 3);
+            const int bytes = (gin.sh_degree + 1) * (gin.sh_degree + 1) * 12;
+            for (int off = 0; off < bytes; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + off));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + bytes - 1));
+        }
+#endif
+        float Sig[9];
+        get_sig(Sig);
+        float A[9], Sv[9];
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                const float col[3] = {Sig[c], Sig[3 + c], Sig[6 + c]};
+                A[3 * a + c] = dot3(cam.R + 3 * a, col);
+            }
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+#pragma unroll
+            for (int c = 0; c < 3; c++) Sv[3 * a + c] = dot3(A + 3 * a, cam.R + 3 * c);
+        // N4
+        const float lx = mul(1.3f, dv(mul(0.5f, (float)cam.W), cam.fx));
+        const float ly = mul(1.3f, dv(mul(0.5f, (float)cam.H), cam.fy));
+        const float tx = mul(fminf(fmaxf(xz, -lx), lx), pv[2]);
+        const float ty = mul(fminf(fmaxf(yz, -ly), ly), pv[2]);
+        const float zz2 = mul(pv[2], pv[2]);
+        const float J0[3] = {dv(cam.fx, pv[2]), 0.0f, -dv(mul(cam.fx, tx), zz2)};
+        const float J1[3] = {0.0f, dv(cam.fy, pv[2]), -dv(mul(cam.fy, ty), zz2)};
+        float B0[3], B1[3];
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            const float col[3] = {Sv[c], Sv[3 + c], Sv[6 + c]};
+            B0[c] = dot3(J0, col);
+            B1[c] = dot3(J1, col);
+        }
+        const float ca_ = add(dot3(B0, J0), dilation), cb_ = dot3(B0, J1), cc_ = add(dot3(B1, J1), dilation);
+        const float det = fma_(ca_, cc_, -mul(cb_, cb_));
+        if (!(det > 0.0f)) break;
+        const float inv = dv(1.0f, det);
+        const float ka = mul(cc_, inv), kb = mul(-cb_, inv), kc = mul(ca_, inv);
+        if (!(ka > 0.0f && fma_(ka, kc, -mul(kb, kb)) > 0.0f)) break;
+        // N5
+        if (!(255.0 * (double)o >= 1.0)) break;
+        const float qmax = (float)(2.0 * log(255.0 * (double)o));
+        const float ex = fma_(__fsqrt_rn(mul(qmax, ca_)), 1.0009765625f, 0.00390625f);
+        const float ey = fma_(__fsqrt_rn(mul(qmax, cc_)), 1.0009765625f, 0.00390625f);
+        const float flx = floorf(mul(sub(u, ex), 0.0625f)), fhx = floorf(mul(add(u, ex), 0.0625f));
+        const float fly = floorf(mul(sub(v, ey), 0.0625f)), fhy = floorf(mul(add(v, ey), 0.0625f));
+        if (!(fhx >= 0.0f && flx <= (float)(cam.tiles_x - 1) && fhy >= 0.0f && fly <= (float)(cam.tiles_y - 1)))
+            break;
+        const int x0 = (int)fmaxf(flx, 0.0f), x1 = (int)fminf(fhx, (float)(cam.tiles_x - 1));
+        const int y0 = (int)fmaxf(fly, 0.0f), y1 = (int)fminf(fhy, (float)(cam.tiles_y - 1));
+        touched = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+        // colour: SH at normalize(mu - campos)
+        float dxw = mx - cam.campos[0], dyw = my - cam.campos[1], dzw = mz - cam.campos[2];
+        const float rn = rsqrtf(dxw * dxw + dyw * dyw + dzw * dzw);
+        float rgb[3];
+        const int kc3 = (gin.sh_degree + 1) * (gin.sh_degree + 1) * 3;
+        sh_eval(gin.sh + g * kc3, gin.sh_degree, dxw * rn, dyw * rn, dzw * rn, rgb);
+        // half-extents of the blend's exact per-warp culling (see blend.cu): the bbox of
+        // {d : Q(d) <= q_max (1 + 0.02)} of the fp32 conic Q, padded; -1 = never cull
+        float cex = -1.f, cey = -1.f;
+        {
+            const float cdet = ka * kc - kb * kb, csum = ka + kc;
+            if (cdet > 0.f && csum * csum <= 1000.f * cdet) {
+                const float ex2 = sqrtf(qmax * kc / cdet) * 1.01f + 0.01f;
+                const float ey2 = sqrtf(qmax * ka / cdet) * 1.01f + 0.01f;
+                if (ex2 < 1e30f && ey2 < 1e30f) { cex = ex2; cey = ey2; }
+            }
+        }
+        GaussRecord rec;
+        rec.a = make_float4(u, v, qmax, o);
+        rec.b = make_float4(ka, kb, kc, cey);
+        rec.c = make_float4(rgb[0], rgb[1], rgb[2], cex);
+        b.grec[g] = rec;
+        b.rect[p] = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 16), (uint32_t)x1 | ((uint32_t)y1 << 16));
+        b.dkey[p] = __float_as_uint(pv[2]);
+        vis = true;
+    } while (0);
+    UNIMGS_CHECK(p < b.st->cap_prims);
+    b.touched[p] = touched;
+    if (!vis) b.dkey[p] = 0xFFFFFFFFu;
+    return vis;
+}
+
+// N3: Sigma = R S^2 R^T from the quaternion (w, x, y, z) and the scales
+__device__ __forceinline__ void sigma_n3(float qw, float qx, float qy, float qz, float s0, float s1, float s2,
+                                         float Sig[9]) {
+    float w = qw, x = qx, y = qy, z = qz;
+    const float n2 = fma_(w, w, fma_(x, x, fma_(y, y, mul(z, z))));
+    const float k = dv(1.0f, __fsqrt_rn(n2));
+    w = mul(w, k); x = mul(x, k); y = mul(y, k); z = mul(z, k);
+    const float qxx = mul(x, x), qyy = mul(y, y), qzz = mul(z, z), qxy = mul(x, y), qxz = mul(x, z),
+                qyz = mul(y, z), qwx = mul(w, x), qwy = mul(w, y), qwz = mul(w, z);
+    float r[9];
+    r[0] = sub(1.0f, mul(2.0f, add(qyy, qzz))); r[1] = mul(2.0f, sub(qxy, qwz)); r[2] = mul(2.0f, add(qxz, qwy));
+    r[3] = mul(2.0f, add(qxy, qwz)); r[4] = sub(1.0f, mul(2.0f, add(qxx, qzz))); r[5] = mul(2.0f, sub(qyz, qwx));
+    r[6] = mul(2.0f, sub(qxz, qwy)); r[7] = mul(2.0f, add(qyz, qwx)); r[8] = sub(1.0f, mul(2.0f, add(qxx, qyy)));
+    float m[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        m[3 * a] = mul(r[3 * a], s0); m[3 * a + 1] = mul(r[3 * a + 1], s1); m[3 * a + 2] = mul(r[3 * a + 2], s2);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int c = 0; c < 3; c++) Sig[3 * a + c] = dot3(m + 3 * a, m + 3 * c);
+}
+
+__device__ __forceinline__ void sigma_given(const float *cv, float Sig[9]) {
+    Sig[0] = __ldg(cv); Sig[1] = Sig[3] = __ldg(cv + 1); Sig[2] = Sig[6] = __ldg(cv + 2);
+    Sig[4] = __ldg(cv + 3); Sig[5] = Sig[7] = __ldg(cv + 4); Sig[8] = __ldg(cv + 5);
+}
+
 // B1: one thread per Gaussian (N1-N5).
 #ifndef UNIMGS_PRE_MINB
 #define UNIMGS_PRE_MINB 5  // 48 registers: 5 CTAs per SM
 #endif
-__global__ void __launch_bounds__(256, UNIMGS_PRE_MINB) k_preprocess_gaussians(GaussInput gin, int64_t F, CamParams cam, float dilation,
-                                                             Buffers b) {
+__global__ void __launch_bounds__(256, UNIMGS_PRE_MINB) k_preprocess_gaussians(GaussInput gin, int64_t F, CamParams cam,
+                                                                               float dilation, Buffers b) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool vis = false;
     if (g < gin.N) {
-        const int64_t p = F + g;
         uint32_t touched = 0;
         // all per-Gaussian inputs except SH are loaded up front (one round trip)
         const float mx = __ldg(gin.means + 3 * g), my = __ldg(gin.means + 3 * g + 1), mz = __ldg(gin.means + 3 * g + 2);
@@ -132,127 +266,64 @@ __global__ void __launch_bounds__(256, UNIMGS_PRE_MINB) k_preprocess_gaussians(G
         const float s0 = qs ? __ldg(gin.scales + 3 * g) : 0.f, s1 = qs ? __ldg(gin.scales + 3 * g + 1) : 0.f,
                     s2 = qs ? __ldg(gin.scales + 3 * g + 2) : 0.f;
         const float o = __ldg(gin.opac + g);
-        do {
-            float pv[3];
-            view_point(cam, mx, my, mz, pv);
-            if (!(pv[2] > cam.near_z) || pv[2] > cam.far_z) break;
-            const float xz = dv(pv[0], pv[2]), yz = dv(pv[1], pv[2]);          // N2
-            const float u = fma_(cam.fx, xz, cam.cx), v = fma_(cam.fy, yz, cam.cy);
-#if UNIMGS_SH_PREFETCH
-            // likely visible: start pulling its SH coefficients into L2 now, so the
-            // EWA math below hides the latency of the dependent SH loads
-            if (u > -(float)cam.W && u < 2.f * (float)cam.W && v > -(float)cam.H && v < 2.f * (float)cam.H) {
-                const char *shp = reinterpret_cast<const char *>(gin.sh + g * (gin.sh_degree + 1) * (gin.sh_degree + 1) * 3);
-                const int bytes = (gin.sh_degree + 1) * (gin.sh_degree + 1) * 12;
-                for (int off = 0; off < bytes; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + off));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + bytes - 1));
-            }
-#endif
-            float Sig[9];
-            if (gin.cov3d) {  // given covariance (e.g. from the deformation transfer)
-                const float *cv = gin.cov3d + 6 * g;
-                Sig[0] = __ldg(cv); Sig[1] = Sig[3] = __ldg(cv + 1); Sig[2] = Sig[6] = __ldg(cv + 2);
-                Sig[4] = __ldg(cv + 3); Sig[5] = Sig[7] = __ldg(cv + 4); Sig[8] = __ldg(cv + 5);
-            } else {
-            // N3
-            float w = qw, x = qx, y = qy, z = qz;
-            const float n2 = fma_(w, w, fma_(x, x, fma_(y, y, mul(z, z))));
-            const float k = dv(1.0f, __fsqrt_rn(n2));
-            w = mul(w, k); x = mul(x, k); y = mul(y, k); z = mul(z, k);
-            const float qxx = mul(x, x), qyy = mul(y, y), qzz = mul(z, z), qxy = mul(x, y), qxz = mul(x, z),
-                        qyz = mul(y, z), qwx = mul(w, x), qwy = mul(w, y), qwz = mul(w, z);
-            float r[9];
-            r[0] = sub(1.0f, mul(2.0f, add(qyy, qzz))); r[1] = mul(2.0f, sub(qxy, qwz)); r[2] = mul(2.0f, add(qxz, qwy));
-            r[3] = mul(2.0f, add(qxy, qwz)); r[4] = sub(1.0f, mul(2.0f, add(qxx, qzz))); r[5] = mul(2.0f, sub(qyz, qwx));
-            r[6] = mul(2.0f, sub(qxz, qwy)); r[7] = mul(2.0f, add(qyz, qwx)); r[8] = sub(1.0f, mul(2.0f, add(qxx, qyy)));
-            float m[9];
-#pragma unroll
-            for (int a = 0; a < 3; a++) {
-                m[3 * a] = mul(r[3 * a], s0); m[3 * a + 1] = mul(r[3 * a + 1], s1); m[3 * a + 2] = mul(r[3 * a + 2], s2);
-            }
-#pragma unroll
-            for (int a = 0; a < 3; a++)
-#pragma unroll
-                for (int c = 0; c < 3; c++) Sig[3 * a + c] = dot3(m + 3 * a, m + 3 * c);
-            }
-            float A[9], Sv[9];
-#pragma unroll
-            for (int a = 0; a < 3; a++)
-#pragma unroll
-                for (int c = 0; c < 3; c++) {
-                    const float col[3] = {Sig[c], Sig[3 + c], Sig[6 + c]};
-                    A[3 * a + c] = dot3(cam.R + 3 * a, col);
-                }
-#pragma unroll
-            for (int a = 0; a < 3; a++)
-#pragma unroll
-                for (int c = 0; c < 3; c++) Sv[3 * a + c] = dot3(A + 3 * a, cam.R + 3 * c);
-            // N4
-            const float lx = mul(1.3f, dv(mul(0.5f, (float)cam.W), cam.fx));
-            const float ly = mul(1.3f, dv(mul(0.5f, (float)cam.H), cam.fy));
-            const float tx = mul(fminf(fmaxf(xz, -lx), lx), pv[2]);
-            const float ty = mul(fminf(fmaxf(yz, -ly), ly), pv[2]);
-            const float zz2 = mul(pv[2], pv[2]);
-            const float J0[3] = {dv(cam.fx, pv[2]), 0.0f, -dv(mul(cam.fx, tx), zz2)};
-            const float J1[3] = {0.0f, dv(cam.fy, pv[2]), -dv(mul(cam.fy, ty), zz2)};
-            float B0[3], B1[3];
-#pragma unroll
-            for (int c = 0; c < 3; c++) {
-                const float col[3] = {Sv[c], Sv[3 + c], Sv[6 + c]};
-                B0[c] = dot3(J0, col);
-                B1[c] = dot3(J1, col);
-            }
-            const float ca_ = add(dot3(B0, J0), dilation), cb_ = dot3(B0, J1), cc_ = add(dot3(B1, J1), dilation);
-            const float det = fma_(ca_, cc_, -mul(cb_, cb_));
-            if (!(det > 0.0f)) break;
-            const float inv = dv(1.0f, det);
-            const float ka = mul(cc_, inv), kb = mul(-cb_, inv), kc = mul(ca_, inv);
-            if (!(ka > 0.0f && fma_(ka, kc, -mul(kb, kb)) > 0.0f)) break;
-            // N5
-            if (!(255.0 * (double)o >= 1.0)) break;
-            const float qmax = (float)(2.0 * log(255.0 * (double)o));
-            const float ex = fma_(__fsqrt_rn(mul(qmax, ca_)), 1.0009765625f, 0.00390625f);
-            const float ey = fma_(__fsqrt_rn(mul(qmax, cc_)), 1.0009765625f, 0.00390625f);
-            const float flx = floorf(mul(sub(u, ex), 0.0625f)), fhx = floorf(mul(add(u, ex), 0.0625f));
-            const float fly = floorf(mul(sub(v, ey), 0.0625f)), fhy = floorf(mul(add(v, ey), 0.0625f));
-            if (!(fhx >= 0.0f && flx <= (float)(cam.tiles_x - 1) && fhy >= 0.0f && fly <= (float)(cam.tiles_y - 1)))
-                break;
-            const int x0 = (int)fmaxf(flx, 0.0f), x1 = (int)fminf(fhx, (float)(cam.tiles_x - 1));
-            const int y0 = (int)fmaxf(fly, 0.0f), y1 = (int)fminf(fhy, (float)(cam.tiles_y - 1));
-            touched = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
-            // colour: SH at normalize(mu - campos)
-            float dxw = mx - cam.campos[0], dyw = my - cam.campos[1], dzw = mz - cam.campos[2];
-            const float rn = rsqrtf(dxw * dxw + dyw * dyw + dzw * dzw);
-            float rgb[3];
-            const int kc3 = (gin.sh_degree + 1) * (gin.sh_degree + 1) * 3;
-            sh_eval(gin.sh + g * kc3, gin.sh_degree, dxw * rn, dyw * rn, dzw * rn, rgb);
-            // half-extents of the blend's exact per-warp culling (see blend.cu): the bbox of
-            // {d : Q(d) <= q_max (1 + 0.02)} of the fp32 conic Q, padded; -1 = never cull
-            float cex = -1.f, cey = -1.f;
-            {
-                const float cdet = ka * kc - kb * kb, csum = ka + kc;
-                if (cdet > 0.f && csum * csum <= 1000.f * cdet) {
-                    const float ex2 = sqrtf(qmax * kc / cdet) * 1.01f + 0.01f;
-                    const float ey2 = sqrtf(qmax * ka / cdet) * 1.01f + 0.01f;
-                    if (ex2 < 1e30f && ey2 < 1e30f) { cex = ex2; cey = ey2; }
-                }
-            }
-            GaussRecord rec;
-            rec.a = make_float4(u, v, qmax, o);
-            rec.b = make_float4(ka, kb, kc, cey);
-            rec.c = make_float4(rgb[0], rgb[1], rgb[2], cex);
-            b.grec[g] = rec;
-            b.rect[p] = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 16), (uint32_t)x1 | ((uint32_t)y1 << 16));
-            b.dkey[p] = __float_as_uint(pv[2]);
-            vis = true;
-        } while (0);
-        UNIMGS_CHECK(p < b.st->cap_prims);
-        b.touched[p] = touched;
-        if (!vis) b.dkey[p] = 0xFFFFFFFFu;
+        vis = project_gaussian(gin, g, F, cam, dilation, b, mx, my, mz, o, touched, [&](float Sig[9]) {
+            if (gin.cov3d) sigma_given(gin.cov3d + 6 * g, Sig);  // given covariance (e.g. deformation transfer)
+            else sigma_n3(qw, qx, qy, qz, s0, s1, s2, Sig);
+        });
     }
     const unsigned cnt = __popc(__ballot_sync(0xffffffffu, vis));
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&b.st->vis_g, cnt);
     block_count(vis, b.bcnt + (F + 255) / 256 + blockIdx.x);
+}
+
+// B1 for several views of one scene (unimgs_preprocess_multi): every Gaussian's
+// inputs -- and Sigma (N3) -- are read / computed once and projected into each view's
+// context; the SH coefficients are re-read per view from L1 / L2.  Per view the
+// arithmetic is exactly the single-view kernel's, so the records are bit-identical.
+__global__ void __launch_bounds__(256, 4) k_preprocess_gaussians_multi(GaussInput gin, int64_t F,
+                                                                                     MultiView mv, float dilation) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool in = g < gin.N;
+    float mx = 0.f, my = 0.f, mz = 0.f, qw = 1.f, qx = 0.f, qy = 0.f, qz = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f, o = 0.f;
+    if (in) {
+        mx = __ldg(gin.means + 3 * g); my = __ldg(gin.means + 3 * g + 1); mz = __ldg(gin.means + 3 * g + 2);
+        if (!gin.cov3d) {
+            qw = __ldg(gin.quats + 4 * g); qx = __ldg(gin.quats + 4 * g + 1);
+            qy = __ldg(gin.quats + 4 * g + 2); qz = __ldg(gin.quats + 4 * g + 3);
+            s0 = __ldg(gin.scales + 3 * g); s1 = __ldg(gin.scales + 3 * g + 1); s2 = __ldg(gin.scales + 3 * g + 2);
+        }
+        o = __ldg(gin.opac + g);
+    }
+    // Sigma once for all views (the 6 distinct entries; in registers)
+    float Sg[9];
+    if (in) {
+        if (gin.cov3d) sigma_given(gin.cov3d + 6 * g, Sg);
+        else sigma_n3(qw, qx, qy, qz, s0, s1, s2, Sg);
+    }
+    const float c00 = Sg[0], c01 = Sg[1], c02 = Sg[2], c11 = Sg[4], c12 = Sg[5], c22 = Sg[8];
+    for (int v = 0; v < mv.n; v++) {
+        bool vis = false;
+        if (in) {
+            uint32_t touched = 0;
+            vis = project_gaussian(gin, g, F, mv.cam[v], dilation, mv.buf[v], mx, my, mz, o, touched,
+                                   [&](float S[9]) {
+                                       S[0] = c00; S[1] = S[3] = c01; S[2] = S[6] = c02;
+                                       S[4] = c11; S[5] = S[7] = c12; S[8] = c22;
+                                   });
+        }
+        const unsigned cnt = __popc(__ballot_sync(0xffffffffu, vis));
+        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&mv.buf[v].st->vis_g, cnt);
+        block_count(vis, mv.buf[v].bcnt + (F + 255) / 256 + blockIdx.x);
+        __syncthreads();  // block_count's shared counters are reused by the next view
+    }
+}
+
+int launch_preprocess_gaussians_multi(const GaussInput &g, int64_t F, const MultiView &mv, float dilation,
+                                      cudaStream_t s) {
+    if (g.N <= 0) return 0;
+    const unsigned blocks = (unsigned)((g.N + 255) / 256);
+    k_preprocess_gaussians_multi<<<blocks, 256, 0, s>>>(g, F, mv, dilation);
+    return 1;
 }
 
 int launch_preprocess_gaussians(const GaussInput &g, int64_t F, const CamParams &cam, float dilation,

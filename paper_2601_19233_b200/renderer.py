@@ -285,27 +285,50 @@ class Renderer:
         return int(self.L.unimgs_launch_count(self._h))
 
 
+def preprocess_multi(renderers: Sequence["Renderer"], scene: DeviceScene, cams: Sequence[SceneCamera], stream=None):
+    """unimgs_preprocess_multi: view v of one scene into renderers[v] (<= 4), the scene read once."""
+    L = _lib.load()
+    n = len(renderers)
+    hs = (C.c_void_p * n)(*[r._h.value for r in renderers])
+    g, m = c_gaussians(scene), c_mesh(scene)
+    arr = (_lib.Camera * n)(*[c_camera(c) for c in cams])
+    rc = L.unimgs_preprocess_multi(hs, n, C.byref(g), C.byref(m), arr, _stream_handle(stream))
+    if rc != _lib.OK:
+        raise _lib.UnimgsError(rc, L.unimgs_error_string(renderers[0]._h).decode())
+    for r, cam in zip(renderers, cams):
+        r._g, r._m, r._cam, r._scene = g, m, cam, scene
+
+
 class ContextPool:
     """Several renderer contexts rendering consecutive views concurrently (the bench's
     launch configuration): view j of a batch goes to context j % n on its
     own stream, so the compute-bound blend of one view overlaps the latency-bound
     binning of the next.  With prio, each context's preprocess + bin run on a
     highest-priority stream and its blend on the normal one; sort_ctas_per_sm = 1 leaves
-    most of each SM to the other contexts' blends."""
+    most of each SM to the other contexts' blends.  With batch > 1, consecutive groups
+    of `batch` views are preprocessed together (unimgs_preprocess_multi: the scene
+    crosses HBM once per group) into one of n / batch context sets, alternating, so a
+    group's preprocess waits only for the blends of the group two back."""
 
     def __init__(self, n: int, max_gaussians: int, max_triangles: int, max_pairs: int, max_w: int, max_h: int,
-                 prio: bool = True, device=None, **settings):
+                 prio: bool = True, device=None, batch: int = 1, **settings):
+        assert batch >= 1 and n % batch == 0
         settings.setdefault("sort_ctas_per_sm", 1 if n > 1 else 0)
+        self.batch = batch
         self.rs = [Renderer(max_gaussians, max_triangles, max_pairs, max_w, max_h, **settings) for _ in range(n)]
         self.streams = [torch.cuda.Stream(device=device) for _ in range(n)]
         # (torch maps a priority beyond the device's range to its highest priority)
         self.pstreams = [torch.cuda.Stream(device=device, priority=-100) for _ in range(n)] if prio else self.streams
+        self.bstreams = [torch.cuda.Stream(device=device, priority=-100 if prio else 0) for _ in range(n // batch)]
+        self.next_set = 0
 
     def render_views(self, scene: DeviceScene, cams: Sequence[SceneCamera], out: torch.Tensor, after=None,
                      ev_pairs=None):
         """Enqueue cams[j] -> out[j] on context j % n.  `after`: a stream every context waits
         on first.  ev_pairs (list): collects (start, end) CUDA events around each blend.
         No join at the end: the caller joins `streams` when it needs the frames."""
+        if self.batch > 1:
+            return self._render_batched(scene, cams, out, after, ev_pairs)
         n = len(self.rs)
         if after is not None:
             for st in self.streams:
@@ -326,6 +349,33 @@ class ContextPool:
                 ev_pairs.append((e0, e1))
             else:
                 rr.render(out[j], stream=ss)
+
+    def _render_batched(self, scene, cams, out, after, ev_pairs):
+        B, nsets = self.batch, len(self.rs) // self.batch
+        if after is not None:
+            for st in self.streams:
+                st.wait_stream(after)
+        for g0 in range(0, len(cams), B):
+            k = self.next_set
+            self.next_set = (k + 1) % nsets
+            idx = list(range(k * B, k * B + min(B, len(cams) - g0)))
+            bs = self.bstreams[k]
+            for i in idx:
+                bs.wait_stream(self.streams[i])  # the set's previous blends have released its buffers
+            preprocess_multi([self.rs[i] for i in idx], scene, cams[g0:g0 + len(idx)], stream=bs)
+            for jj, i in enumerate(idx):
+                rr, ss, ps = self.rs[i], self.streams[i], self.pstreams[i]
+                ps.wait_stream(bs)
+                rr.bin(stream=ps)
+                ss.wait_stream(ps)
+                if ev_pairs is not None:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(ss)
+                    rr.render(out[g0 + jj], stream=ss)
+                    e1.record(ss)
+                    ev_pairs.append((e0, e1))
+                else:
+                    rr.render(out[g0 + jj], stream=ss)
 
     def join(self, stream):
         for st in self.streams:

@@ -73,7 +73,7 @@ def test_no_device_calls_fail_cleanly_without_gpu():
 @pytest.mark.parametrize("field,value,code", [
     ("msaa_samples", 3, "ERR_UNSUPPORTED"), ("blend_mode", 5, "ERR_UNSUPPORTED"),
     ("tile_size", 8, "ERR_UNSUPPORTED"), ("sort_mode", 2, "ERR_UNSUPPORTED"),
-    ("tri_depth", 2, "ERR_UNSUPPORTED"), ("sort_ctas_per_sm", 5, "ERR_INVALID_ARGUMENT"),
+    ("tri_depth", 3, "ERR_UNSUPPORTED"), ("sort_ctas_per_sm", 5, "ERR_INVALID_ARGUMENT"),
     ("sort_ctas_per_sm", -1, "ERR_INVALID_ARGUMENT"), ("alpha_max", 0.0, "ERR_INVALID_ARGUMENT"),
     ("t_eps", 1.0, "ERR_INVALID_ARGUMENT"), ("dilation", -0.1, "ERR_INVALID_ARGUMENT"),
 ])
