@@ -387,18 +387,35 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
             int e = 0;  // largest e < m with s_off[e] <= k0
             for (int step = 1 << (31 - __clz(m)); step >= 1; step >>= 1)
                 if (e + step < m && s_off[e + step] <= k0) e += step;
+            // the first slot's tile by one division, the rest by walking the rectangle
+            // row-major (a primitive change lands on its first slot: local 0)
+            unsigned x0, x1, tx, ty;
+            uint32_t pid;
+            {
+                const uint2 rr = s_rect[e];
+                x0 = rr.x & 0xFFFF, x1 = rr.y & 0xFFFF;
+                const unsigned w = x1 - x0 + 1, local = (unsigned)(k0 - s_off[e]);
+                const unsigned qq = local / w;
+                tx = x0 + (local - qq * w), ty = (rr.x >> 16) + qq;
+                pid = s_id[e];
+            }
             for (int q = 0; q < PER; q++) {
                 const int k = k0 + q;
                 if (k >= (int)ns) break;
-                while (s_off[e + 1] <= k) e++;
-                const uint2 rr = s_rect[e];
-                const unsigned x0 = rr.x & 0xFFFF, y0 = rr.x >> 16, x1 = rr.y & 0xFFFF;
-                const unsigned w = x1 - x0 + 1, local = (unsigned)(k - s_off[e]);
-                const unsigned qq = local / w;
-                const unsigned tx = x0 + (local - qq * w), ty = y0 + qq;
+                if (q > 0) {
+                    if (s_off[e + 1] <= k) {
+                        while (s_off[e + 1] <= k) e++;
+                        const uint2 rr = s_rect[e];
+                        x0 = tx = rr.x & 0xFFFF, x1 = rr.y & 0xFFFF, ty = rr.x >> 16;
+                        pid = s_id[e];
+                    } else if (++tx > x1) {
+                        tx = x0;
+                        ty++;
+                    }
+                }
                 const unsigned t = ty * (unsigned)tiles_x + tx;
-                UNIMGS_CHECK(e < m && t < st->cap_tiles && S + (unsigned)k < st->cap_pairs);
-                const uint32_t pid = s_id[e];
+                UNIMGS_CHECK(e < m && t < st->cap_tiles && S + (unsigned)k < st->cap_pairs &&
+                             (unsigned)(k - s_off[e]) == (ty - (s_rect[e].x >> 16)) * (x1 - x0 + 1) + (tx - x0));
                 if (FULL) {
                     uint32_t d = s_dk[FULL ? e : 0];
                     if (tri_depth && pid < F) {  // N8 per-tile triangle depth
