@@ -33,6 +33,7 @@
 // {epoch tag << 2 | flag, value}; the tag changes every pass of every frame, so
 // nothing is cleared between frames and the whole frame is graph-capturable.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "internal.cuh"
@@ -993,10 +994,42 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2 *__restrict__ r
     for (int i = threadIdx.x; i < tiles; i += blockDim.x) order[atomicAdd(&s_h[bucket(ranges[i])], 1u)] = (uint32_t)i;
 }
 
+// Per-kernel device times of one launch_bin call (UNIMGS_BIN_EVENTS=1: events after
+// every launch on the bin stream, printed to stderr; a diagnostic that synchronises).
+struct BinMarks {
+    bool on = false;
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev[48];
+    const char *name[48];
+    int n = 0;
+    explicit BinMarks(cudaStream_t st) : s(st) {
+        static const bool en = getenv("UNIMGS_BIN_EVENTS") != nullptr;
+        on = en;
+        if (on) mark("start");
+    }
+    void mark(const char *nm) {
+        if (!on || n >= 48) return;
+        cudaEventCreate(&ev[n]);
+        cudaEventRecord(ev[n], s);
+        name[n++] = nm;
+    }
+    ~BinMarks() {
+        if (!on) return;
+        cudaEventSynchronize(ev[n - 1]);
+        for (int i = 1; i < n; i++) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            fprintf(stderr, "bin_event %s %.4f\n", name[i], ms);
+        }
+        for (int i = 0; i < n; i++) cudaEventDestroy(ev[i]);
+    }
+};
+
 int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam, int sort_mode, int tri_depth,
                cudaStream_t s, int sm_count, int sort_per_sm) {
     (void)N;
     int launches = 0;
+    BinMarks mk(s);
     const int64_t tiles = (int64_t)cam.tiles_x * cam.tiles_y;
     const int tb = bits_for(tiles);
     const bool full = sort_mode == 1;
@@ -1007,6 +1040,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         k_scan_counts<<<1, 1024, 0, s>>>(b.bcnt, nbt + nbg, 0, 0, b.st);
         k_compact<<<nbt + nbg, 256, 0, s>>>(F, N, nbt, b.touched, b.dkey, b.bcnt, b.pk[0], b.pv[0], b.st);
         launches += 2;
+        mk.mark("scan+compact");
     }
     int slot = SLOT_PASS0;
     const int dgrid = (int)std::max<int64_t>(1, (P + kScanTile - 1) / kScanTile);
@@ -1018,6 +1052,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         // there -- measured: bench +0.5%, but single-stream bin +3% mip360, +13% nerf)
         k_hist_depth<<<sm_count * 2, 256, 0, s>>>(b.pk[0], b.st);
         launches++;
+        mk.mark("hist_depth");
         const int g1 = sort_grid(P, sm_count, sort_per_sm, kSortThreads * kDepthItems);
         int cur = 0;
         for (int pass = 0; pass < 4; pass++, slot++) {
@@ -1025,6 +1060,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
                                                  8 * pass, 8, HIST_DEPTH0 + pass, slot, g1, s);
             cur ^= 1;
             launches++;
+            mk.mark("depth_onesweep");
         }
         dup_ids = b.pv[cur];
     } else {
@@ -1035,11 +1071,13 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
     k_dup_count<<<dgrid, kScanThreads, 0, s>>>(dup_ids, b.touched, b.dcnt, prel, b.st);
     k_scan_counts<<<1, 1024, 0, s>>>(b.dcnt, dgrid, 1, b.max_pairs, b.st);
     launches += 2;
+    mk.mark("dup_count+scan");
     {
         const int slots = full ? ExpandCfg<true>::SLOTS : ExpandCfg<false>::SLOTS;
         k_range_starts<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, sm_count * 16)), 256, 0,
                          s>>>(b.dcnt, prel, slots, b.rstart, b.st);
         launches++;
+        mk.mark("range_starts");
     }
     const int egrid = (int)std::max<int64_t>(1, std::min<int64_t>((b.max_pairs + 1023) / 1024, sm_count * UNIMGS_EXPAND_PER_SM));
     const int g2 = sort_grid(b.max_pairs, sm_count, sort_per_sm);
@@ -1051,6 +1089,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
                                                         b.trec, (unsigned)F, 0, lo_bits, b.tk[0], b.tv[0], b.tcnt,
                                                         b.st);
         launches++;
+        mk.mark("expand");
         // reduce-then-scan passes (k_expand wrote the first pass's per-tile counts)
         const int ntile_max = (int)((b.max_pairs + kSortTile - 1) / kSortTile);
         const int ngroup_max = (ntile_max + kRtsGroup - 1) / kRtsGroup;
@@ -1074,8 +1113,10 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
                 UNIMGS_NB_SWITCH(UNIMGS_TC)
 #undef UNIMGS_TC
                 launches++;
+                mk.mark("tile_count");
             }
             k_rts_scan<<<ngroup_max, 256, 0, s>>>(b.tcnt, b.gsum, &b.st->K, ngroup_max, SLOT_RTS0 + pass, b.st);
+            mk.mark("rts_scan");
             const size_t smem = onesweep_smem<uint16_t, kSortItems>();
 #define UNIMGS_DS(NB)                                                                                          \
     k_downsweep<uint16_t, kSortItems, NB><<<g2, kSortThreads, smem, s>>>(kin, b.tv[tc], (uint16_t *)b.tk[tc ^ 1], \
@@ -1085,12 +1126,14 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
 #undef UNIMGS_DS
 #undef UNIMGS_NB_SWITCH
             launches += 2;
+            mk.mark("downsweep");
             sh += nb;
             tc ^= 1;
         }
         b.key_bytes = 2;
         k_ranges16<<<sm_count * 4, 256, 0, s>>>((const uint16_t *)b.tk[tc], &b.st->K, b.ranges, b.st);
         launches++;
+        mk.mark("ranges16");
     } else {
         k_expand<true><<<egrid, kScanThreads, 0, s>>>(dup_ids, b.rect, b.dkey, b.dcnt, prel, b.rstart, cam.tiles_x,
                                                        b.trec, (unsigned)F, tri_depth, 8, b.tk[0], b.tv[0], nullptr,
@@ -1112,6 +1155,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
     b.sorted_vals = b.tv[tc];
     k_tile_order<<<1, 1024, 0, s>>>(b.ranges, (int)tiles, b.order, b.st);
     launches++;
+    mk.mark("tile_order");
     return launches;  // kernels only (the ranges memset is not counted)
 }
 

@@ -328,6 +328,11 @@ struct WarpBuf {
 //   4. the packed entries are tested four at a time (two f32x2 pairs) and the
 //      hits blended in list order.
 // No block-wide barrier: a warp stops as soon as all of its pixels have terminated.
+// The (tile, sub-tile) items, in the longest-first tile order (k_tile_order), are
+// dealt to CTAs in runs of items_per_cta (several tiles of similar length); inside a
+// run each warp takes the next item when it is done with its last (a shared-memory
+// counter), so the warps of a CTA end together and an SM slot is not held by one
+// slow sub-tile while its other warps idle.
 #ifndef UNIMGS_BLEND_MINB
 #define UNIMGS_BLEND_MINB 4
 #endif
@@ -338,33 +343,47 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
                                                                      const GaussRecord *__restrict__ grec,
                                                                      const TriRecord *__restrict__ trec, TexView tv,
                                                                      unsigned F, int W, int H, int tiles_x,
+                                                                     unsigned n_items, int items_per_cta,
                                                                      BlendParams bp, float4 *__restrict__ out,
                                                                      DevState *st, uint4 *__restrict__ frag_counts) {
     if (st->overflow) return;
     constexpr int NW = kBlendThreads / 32;  // warps per tile
-    // COUNT only: per lane (= per pixel) Gaussian / triangle entries tested and fragments
-    // blended, and the unified id of the last fragment blended
-    unsigned long long w_gt = 0, w_gf = 0, w_tt = 0, w_tf = 0;
-    unsigned last_id = 0xFFFFFFFFu;
     __shared__ unsigned s_ids[COUNT ? NW : 1][32];  // COUNT only: packed entry k's id
     __shared__ WarpBuf s_buf[NW];
     __shared__ float4 s_stage[NW][32][3];  // this lane's record of the next chunk (cp.async)
     __shared__ TriAttr s_tri[NW][32];      // a packed triangle entry's q2..q5 (cp.async)
+    __shared__ int s_next;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tile = (int)__ldg(order + blockIdx.x);  // longest-first schedule (k_tile_order)
-    const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int sx0 = tx * kTile + (warp & 1) * 8, sy0 = ty * kTile + (warp >> 1) * 4;
-    const int x = sx0 + (lane & 7), y = sy0 + (lane >> 3);
-    const float px = (float)x + 0.5f;
-    const uint2 rg = ranges[tile];
-    UNIMGS_CHECK((unsigned)tile < st->cap_tiles && rg.x <= rg.y && rg.y <= st->K);
     const unsigned lt = (1u << lane) - 1u;
     WarpBuf &wb = s_buf[warp];
     float *ef = &wb.e[0][0].x;
     TriAttr *tat = s_tri[warp];
     float4 *stg = s_stage[warp][lane];
     const unsigned stg_s = (unsigned)__cvta_generic_to_shared(stg);
+    if (threadIdx.x == 0) s_next = 0;
+    __syncthreads();
+
+    for (;;) {
+    unsigned item = 0xFFFFFFFFu;
+    if (lane == 0) {
+        const int j = atomicAdd(&s_next, 1);
+        if (j < items_per_cta) item = blockIdx.x * (unsigned)items_per_cta + (unsigned)j;
+    }
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    const int sub = (int)(item % NW);
+    // COUNT only: per lane (= per pixel) Gaussian / triangle entries tested and fragments
+    // blended, and the unified id of the last fragment blended
+    unsigned long long w_gt = 0, w_gf = 0, w_tt = 0, w_tf = 0;
+    unsigned last_id = 0xFFFFFFFFu;
+    const int tile = (int)__ldg(order + item / NW);  // longest-first schedule (k_tile_order)
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int sx0 = tx * kTile + (sub & 1) * 8, sy0 = ty * kTile + (sub >> 1) * 4;
+    const int x = sx0 + (lane & 7), y = sy0 + (lane >> 3);
+    const float px = (float)x + 0.5f;
+    const uint2 rg = ranges[tile];
+    UNIMGS_CHECK((unsigned)tile < st->cap_tiles && rg.x <= rg.y && rg.y <= st->K);
 
     Px<MODE, M> s;
     s.C0 = s.C1 = s.C2 = 0.f;
@@ -597,6 +616,8 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
         const float T = (MODE == MODE_WHOLE_PIXEL && s.open) ? s.exit_T() : s.T;
         const float sb = T * bp.bg_alpha;
         out[(size_t)y * W + x] = make_float4(s.C0 + sb * bp.bg[0], s.C1 + sb * bp.bg[1], s.C2 + sb * bp.bg[2], T);
+    }
+    __syncwarp();  // the warp's buffers are reused by its next item
     }
 }
 
@@ -911,20 +932,35 @@ static void launch_resort(const Buffers &b, const MeshInput &m, const CamParams 
         reinterpret_cast<float4 *>(out), b.st, reinterpret_cast<uint4 *>(fc));
 }
 
+// k_blend's per-CTA item budget (UNIMGS_BLEND_ITEMS overrides it for experiments):
+// 8 = one tile per CTA, as a plain grid; more lets a CTA's warps balance several tiles.
+static int blend_items_per_cta() {
+    static const int v = [] {
+        const char *e = getenv("UNIMGS_BLEND_ITEMS");
+        const int n = e ? atoi(e) : 0;
+        return n >= 1 ? n : 16;
+    }();
+    return v;
+}
+
 template <int MODE, int M>
 static void launch_mode(const Buffers &b, const MeshInput &m, const CamParams &cam, const BlendParams &bp, float *out,
                         cudaStream_t s, bool count_work, uint32_t *frag_counts) {
     const int tiles = cam.tiles_x * cam.tiles_y;
+    const unsigned n_items = (unsigned)tiles * (kBlendThreads / 32);
+    const int per_cta = blend_items_per_cta();
+    const unsigned grid = (n_items + per_cta - 1) / per_cta;
     TexView tv{reinterpret_cast<const uchar4 *>(m.tex), m.tw, m.th};
     if (count_work)
-        k_blend<true, MODE, M><<<tiles, kBlendThreads, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
-                                                                        (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
-                                                                        reinterpret_cast<float4 *>(out), b.st,
-                                                                        reinterpret_cast<uint4 *>(frag_counts));
+        k_blend<true, MODE, M><<<grid, kBlendThreads, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
+                                                               (unsigned)m.F, cam.W, cam.H, cam.tiles_x, n_items,
+                                                               per_cta, bp, reinterpret_cast<float4 *>(out), b.st,
+                                                               reinterpret_cast<uint4 *>(frag_counts));
     else
-        k_blend<false, MODE, M><<<tiles, kBlendThreads, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
-                                                                         (unsigned)m.F, cam.W, cam.H, cam.tiles_x, bp,
-                                                                         reinterpret_cast<float4 *>(out), b.st, nullptr);
+        k_blend<false, MODE, M><<<grid, kBlendThreads, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
+                                                                (unsigned)m.F, cam.W, cam.H, cam.tiles_x, n_items,
+                                                                per_cta, bp, reinterpret_cast<float4 *>(out), b.st,
+                                                                nullptr);
 }
 
 template <int MODE>
