@@ -12,6 +12,9 @@
 #ifndef UNIMGS_SH_PREFETCH
 #define UNIMGS_SH_PREFETCH 1
 #endif
+#ifndef UNIMGS_SH_PF_MARGIN
+#define UNIMGS_SH_PF_MARGIN 0.25f // prefetch window: the image grown by this fraction on every side
+#endif
 
 namespace unimgs {
 
@@ -133,7 +136,8 @@ __device__ __forceinline__ bool project_gaussian(const GaussInput &gin, int64_t 
 #if UNIMGS_SH_PREFETCH
         // likely visible: start pulling its SH coefficients into L2 now, so the
         // EWA math below hides the latency of the dependent SH loads
-        if (u > -(float)cam.W && u < 2.f * (float)cam.W && v > -(float)cam.H && v < 2.f * (float)cam.H) {
+        if (u > -UNIMGS_SH_PF_MARGIN * (float)cam.W && u < (1.f + UNIMGS_SH_PF_MARGIN) * (float)cam.W &&
+            v > -UNIMGS_SH_PF_MARGIN * (float)cam.H && v < (1.f + UNIMGS_SH_PF_MARGIN) * (float)cam.H) {
             const char *shp = reinterpret_cast<const char *>(gin.sh + g * (gin.sh_degree + 1) * (gin.sh_degree + 1) * 3);
             const int bytes = (gin.sh_degree + 1) * (gin.sh_degree + 1) * 12;
             for (int off = 0; off < bytes; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + off));
@@ -249,10 +253,13 @@ __device__ __forceinline__ void sigma_given(const float *cv, float Sig[9]) {
 }
 
 // B1: one thread per Gaussian (N1-N5).
-#ifndef UNIMGS_PRE_MINB
-#define UNIMGS_PRE_MINB 5  // 48 registers: 5 CTAs per SM
+#ifndef UNIMGS_PRE_THREADS
+#define UNIMGS_PRE_THREADS 64  // small CTAs: the SM slot of a finished CTA is refilled at once
 #endif
-__global__ void __launch_bounds__(256, UNIMGS_PRE_MINB) k_preprocess_gaussians(GaussInput gin, int64_t F, CamParams cam,
+#ifndef UNIMGS_PRE_MINB
+#define UNIMGS_PRE_MINB (5 * 256 / UNIMGS_PRE_THREADS)  // 48 registers
+#endif
+__global__ void __launch_bounds__(UNIMGS_PRE_THREADS, UNIMGS_PRE_MINB) k_preprocess_gaussians(GaussInput gin, int64_t F, CamParams cam,
                                                                                float dilation, Buffers b) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool vis = false;
@@ -271,9 +278,13 @@ __global__ void __launch_bounds__(256, UNIMGS_PRE_MINB) k_preprocess_gaussians(G
             else sigma_n3(qw, qx, qy, qz, s0, s1, s2, Sig);
         });
     }
+    // per-warp counts into the (zeroed) count of the Gaussian's 256-run: no CTA
+    // barrier, so a CTA retires as soon as its warps are done
     const unsigned cnt = __popc(__ballot_sync(0xffffffffu, vis));
-    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&b.st->vis_g, cnt);
-    block_count(vis, b.bcnt + (F + 255) / 256 + blockIdx.x);
+    if ((threadIdx.x & 31) == 0 && cnt) {
+        atomicAdd(&b.st->vis_g, cnt);
+        atomicAdd(b.bcnt + (F + 255) / 256 + (g >> 8), cnt);
+    }
 }
 
 // B1 for several views of one scene (unimgs_preprocess_multi): every Gaussian's
@@ -329,7 +340,8 @@ int launch_preprocess_gaussians_multi(const GaussInput &g, int64_t F, const Mult
 int launch_preprocess_gaussians(const GaussInput &g, int64_t F, const CamParams &cam, float dilation,
                                 const Buffers &b, cudaStream_t s) {
     if (g.N <= 0) return 0;
-    const int threads = 256;
+    cudaMemsetAsync(b.bcnt + (F + 255) / 256, 0, sizeof(uint32_t) * (size_t)((g.N + 255) / 256), s);
+    const int threads = UNIMGS_PRE_THREADS;  // a divisor of 256 (the count runs)
     const unsigned blocks = (unsigned)((g.N + threads - 1) / threads);
     k_preprocess_gaussians<<<blocks, threads, 0, s>>>(g, F, cam, dilation, b);
     return 1;
