@@ -94,7 +94,7 @@ __device__ __forceinline__ unsigned claim_tile(unsigned *ctr, unsigned *s_tile) 
 
 // ----------------------------------------------------------------------------
 // Reduce-then-scan (no look-back chains):
-//   B1/B2 write one visible count per CTA of 256 primitives (bcnt);
+//   B2 / B1 write one visible count per run of 256 triangles / kGaussRun Gaussians (bcnt);
 //   k_scan_counts scans a count array in place in one CTA;
 //   k_compact writes every visible primitive at its CTA offset + local rank;
 //   k_dup_count / k_scan_counts / k_expand do the same for the pairs.
@@ -159,33 +159,47 @@ __global__ void __launch_bounds__(1024) k_scan_counts(uint32_t *cnt, int64_t n, 
     }
 }
 
-// One CTA per 256 primitives, in the block order of B2 (triangles) then B1 (Gaussians).
+// One CTA (256 threads) per count run, triangles first: a run of 256 triangles
+// (B2's counts) or of kGaussRun Gaussians (B1's counts, walked 256 at a time); each
+// visible primitive goes to its run's offset + its rank in the run.
 __global__ void __launch_bounds__(256) k_compact(int64_t F, int64_t N, int nbt, const uint32_t *__restrict__ touched,
                                                  const uint32_t *__restrict__ dkey, const uint32_t *__restrict__ boff,
                                                  uint32_t *ok, uint32_t *ov, const DevState *st) {
-    __shared__ unsigned s_c[8];
+    __shared__ unsigned s_c[2][8];
     const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int blk = blockIdx.x;
-    int64_t p;
-    bool in;
-    if (blk < nbt) {
-        p = (int64_t)blk * 256 + threadIdx.x;
-        in = p < F;
-    } else {
-        const int64_t g = (int64_t)(blk - nbt) * 256 + threadIdx.x;
-        in = g < N;
-        p = F + g;
-    }
-    const bool v = in && touched[p] > 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, v);
-    if (lane == 0) s_c[wid] = __popc(bal);
-    __syncthreads();
-    if (v) {
-        unsigned pos = boff[blk] + __popc(bal & ((1u << lane) - 1u));
-        for (unsigned w = 0; w < wid; w++) pos += s_c[w];
-        UNIMGS_CHECK(pos < st->cap_prims);
-        ok[pos] = dkey[p];
-        ov[pos] = (uint32_t)p;
+    const bool tri = blk < nbt;
+    unsigned base = boff[blk];
+    const int nsub = tri ? 1 : kGaussRun / 256;
+    for (int sub = 0; sub < nsub; sub++) {
+        int64_t p;
+        bool in;
+        if (tri) {
+            p = (int64_t)blk * 256 + threadIdx.x;
+            in = p < F;
+        } else {
+            const int64_t g = (int64_t)(blk - nbt) * kGaussRun + sub * 256 + threadIdx.x;
+            in = g < N;
+            p = F + g;
+        }
+        const bool v = in && touched[p] > 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, v);
+        if (lane == 0) s_c[sub & 1][wid] = __popc(bal);
+        __syncthreads();  // (double-buffered s_c: one barrier per sub-block)
+        unsigned before = 0, total = 0;
+#pragma unroll
+        for (unsigned w = 0; w < 8; w++) {
+            const unsigned c = s_c[sub & 1][w];
+            before += w < wid ? c : 0u;
+            total += c;
+        }
+        if (v) {
+            const unsigned pos = base + before + __popc(bal & ((1u << lane) - 1u));
+            UNIMGS_CHECK(pos < st->cap_prims);
+            ok[pos] = dkey[p];
+            ov[pos] = (uint32_t)p;
+        }
+        base += total;
     }
 }
 
@@ -256,13 +270,21 @@ __global__ void __launch_bounds__(256) k_hist_depth(const uint32_t *__restrict__
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&s_top[0][0])[i] = 0;
     __syncthreads();
     const unsigned n = st->n_vis, wid = threadIdx.x >> 5;
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t k = keys[i];
+    auto add = [&](uint32_t k) {
         atomicAdd(&s_h[k & 255u], 1u);
         atomicAdd(&s_h[256 + ((k >> 8) & 255u)], 1u);
         atomicAdd(&s_h[512 + ((k >> 16) & 255u)], 1u);
         atomicAdd(&s_top[wid][k >> 24], 1u);
+    };
+    // 2 x 16-byte loads in flight per thread and iteration (keys is 16-byte aligned)
+    const unsigned n8 = n / 8;
+    const uint4 *k4 = reinterpret_cast<const uint4 *>(keys);
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
+        const uint4 a = __ldg(k4 + 2 * i), c = __ldg(k4 + 2 * i + 1);
+        add(a.x); add(a.y); add(a.z); add(a.w);
+        add(c.x); add(c.y); add(c.z); add(c.w);
     }
+    for (unsigned i = 8 * n8 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) add(keys[i]);
     __syncthreads();
     for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x)
         if (s_h[i]) atomicAdd(&st->hist[HIST_DEPTH0 + i / 256][i % 256], s_h[i]);
@@ -1035,7 +1057,7 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
     const bool full = sort_mode == 1;
     cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * (size_t)tiles, s);
     // compaction of the visible primitives (B2 then B1 CTA counts)
-    const int nbt = (int)((F + 255) / 256), nbg = (int)((N + 255) / 256);
+    const int nbt = (int)((F + 255) / 256), nbg = (int)((N + kGaussRun - 1) / kGaussRun);
     if (P > 0) {
         k_scan_counts<<<1, 1024, 0, s>>>(b.bcnt, nbt + nbg, 0, 0, b.st);
         k_compact<<<nbt + nbg, 256, 0, s>>>(F, N, nbt, b.touched, b.dkey, b.bcnt, b.pk[0], b.pv[0], b.st);

@@ -26,6 +26,8 @@ namespace unimgs {
 #endif
 
 constexpr int kTile = 16;
+// B1's visible counts (Buffers::bcnt) are per run of kGaussRun Gaussians (B2's: per 256 triangles)
+constexpr int kGaussRunLog2 = 10, kGaussRun = 1 << kGaussRunLog2;
 constexpr int kBlendThreads = 256;
 constexpr int kMaxPasses = 8;
 

@@ -254,7 +254,7 @@ __device__ __forceinline__ void sigma_given(const float *cv, float Sig[9]) {
 
 // B1: one thread per Gaussian (N1-N5).
 #ifndef UNIMGS_PRE_THREADS
-#define UNIMGS_PRE_THREADS 64  // small CTAs: the SM slot of a finished CTA is refilled at once
+#define UNIMGS_PRE_THREADS 64  // small CTAs (a divisor of kGaussRun): a finished CTA's slot is refilled at once
 #endif
 #ifndef UNIMGS_PRE_MINB
 #define UNIMGS_PRE_MINB (5 * 256 / UNIMGS_PRE_THREADS)  // 48 registers
@@ -278,12 +278,12 @@ __global__ void __launch_bounds__(UNIMGS_PRE_THREADS, UNIMGS_PRE_MINB) k_preproc
             else sigma_n3(qw, qx, qy, qz, s0, s1, s2, Sig);
         });
     }
-    // per-warp counts into the (zeroed) count of the Gaussian's 256-run: no CTA
-    // barrier, so a CTA retires as soon as its warps are done
+    // per-warp counts into the (zeroed) count of the Gaussian's run of kGaussRun: no
+    // CTA barrier, so a CTA retires as soon as its warps are done
     const unsigned cnt = __popc(__ballot_sync(0xffffffffu, vis));
     if ((threadIdx.x & 31) == 0 && cnt) {
         atomicAdd(&b.st->vis_g, cnt);
-        atomicAdd(b.bcnt + (F + 255) / 256 + (g >> 8), cnt);
+        atomicAdd(b.bcnt + (F + 255) / 256 + (g >> kGaussRunLog2), cnt);
     }
 }
 
@@ -323,15 +323,19 @@ __global__ void __launch_bounds__(256, 4) k_preprocess_gaussians_multi(GaussInpu
                                    });
         }
         const unsigned cnt = __popc(__ballot_sync(0xffffffffu, vis));
-        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&mv.buf[v].st->vis_g, cnt);
-        block_count(vis, mv.buf[v].bcnt + (F + 255) / 256 + blockIdx.x);
-        __syncthreads();  // block_count's shared counters are reused by the next view
+        if ((threadIdx.x & 31) == 0 && cnt) {
+            atomicAdd(&mv.buf[v].st->vis_g, cnt);
+            atomicAdd(mv.buf[v].bcnt + (F + 255) / 256 + (g >> kGaussRunLog2), cnt);
+        }
     }
 }
 
 int launch_preprocess_gaussians_multi(const GaussInput &g, int64_t F, const MultiView &mv, float dilation,
                                       cudaStream_t s) {
     if (g.N <= 0) return 0;
+    for (int v = 0; v < mv.n; v++)
+        cudaMemsetAsync(mv.buf[v].bcnt + (F + 255) / 256, 0,
+                        sizeof(uint32_t) * (size_t)((g.N + kGaussRun - 1) / kGaussRun), s);
     const unsigned blocks = (unsigned)((g.N + 255) / 256);
     k_preprocess_gaussians_multi<<<blocks, 256, 0, s>>>(g, F, mv, dilation);
     return 1;
@@ -340,8 +344,8 @@ int launch_preprocess_gaussians_multi(const GaussInput &g, int64_t F, const Mult
 int launch_preprocess_gaussians(const GaussInput &g, int64_t F, const CamParams &cam, float dilation,
                                 const Buffers &b, cudaStream_t s) {
     if (g.N <= 0) return 0;
-    cudaMemsetAsync(b.bcnt + (F + 255) / 256, 0, sizeof(uint32_t) * (size_t)((g.N + 255) / 256), s);
-    const int threads = UNIMGS_PRE_THREADS;  // a divisor of 256 (the count runs)
+    cudaMemsetAsync(b.bcnt + (F + 255) / 256, 0, sizeof(uint32_t) * (size_t)((g.N + kGaussRun - 1) / kGaussRun), s);
+    const int threads = UNIMGS_PRE_THREADS;
     const unsigned blocks = (unsigned)((g.N + threads - 1) / threads);
     k_preprocess_gaussians<<<blocks, threads, 0, s>>>(g, F, cam, dilation, b);
     return 1;
