@@ -305,16 +305,18 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
     return r;
 }
 
-// Per-warp packed entry buffer.  Entries 2p and 2p+1 form pair p, stored
-// structure-of-arrays so that one 16-byte shared load yields f32x2 operands:
-//   e[p][0] = {u0, u1, v0, v1}        (triangle: X0, Y0 bits)
-//   e[p][1] = {ca0, ca1, cc0, cc1}    (triangle: X1, Y1 bits)
-//   e[p][2] = {2cb0, 2cb1, qm0, qm1}  (triangle: X2 bits, q_max = -1; padding: NaN)
-//   col[k]  = {r, g, b, log2 o}       (triangle: Y2 bits, kind, alpha, id)
+// Per-warp packed entry buffer.  Entries 2p and 2p+1 form pair p; a pair's 80 bytes
+// are contiguous (one pointer walks the buffer), stored structure-of-arrays so that
+// one 16-byte shared load yields f32x2 operands:
+//   v[p][0] = {u0, u1, v0, v1}        (triangle: X0, Y0 bits)
+//   v[p][1] = {ca0, ca1, cc0, cc1}    (triangle: X1, Y1 bits)
+//   v[p][2] = {2cb0, 2cb1, qm0, qm1}  (triangle: X2 bits, q_max = -1; padding: NaN)
+//   v[p][3 + j] = col(2p + j) = {r, g, b, log2 o}  (triangle: Y2 bits, kind, alpha, id)
 struct WarpBuf {
-    float4 e[16][3];
-    float4 col[32];
+    float4 v[16][5];
+    __device__ __forceinline__ float4 &col(unsigned k) { return v[k >> 1][3 + (k & 1)]; }
 };
+constexpr int kPairFloats = 20;  // floats per pair in WarpBuf
 
 // One CTA per 16x16 tile, 8 independent warps, one pixel per lane.  Warp w owns
 // the 8x4 sub-tile (w & 1, w >> 1) and walks the whole tile list in chunks of 32
@@ -357,7 +359,7 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     WarpBuf &wb = s_buf[warp];
-    float *ef = &wb.e[0][0].x;
+    float *ef = &wb.v[0][0].x;
     TriAttr *tat = s_tri[warp];
     float4 *stg = s_stage[warp][lane];
     const unsigned stg_s = (unsigned)__cvta_generic_to_shared(stg);
@@ -420,7 +422,7 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
             w_gf++;
             last_id = s_ids[COUNT ? warp : 0][k];
         }
-        const float4 ec = wb.col[k];
+        const float4 ec = wb.col(k);
         const float al = fminf(bp.alpha_max, ex2_ftz(fmaf(q, kexp, ec.w)));
         if (MODE == MODE_WHOLE_PIXEL && s.open) {
             // Fig.3b/c: the entity spans the whole list; the Gaussian does not
@@ -443,7 +445,7 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
     //   dx = (x + .5) - u; dy = (y + .5) - v; q = fma(ca, dx dx, fma(cc, dy dy, 2cb (dx dy)))
     // (py is NaN once the pixel is done, so its q is NaN and no test passes)
     auto qpair = [&](unsigned p, float &q0, float &q1, float &m0, float &m1) {
-        const float4 A = wb.e[p][0], B = wb.e[p][1], Cc = wb.e[p][2];
+        const float4 A = wb.v[p][0], B = wb.v[p][1], Cc = wb.v[p][2];
         const f32x2 dx = sub2(pk2(px, px), pk2(A.x, A.y));
         const f32x2 dy = sub2(pk2(s.py, s.py), pk2(A.z, A.w));
         const f32x2 t = fma2(pk2(B.z, B.w), mul2(dy, dy), mul2(pk2(Cc.x, Cc.y), mul2(dx, dy)));
@@ -493,14 +495,14 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
         UNIMGS_CHECK(!rel || (slot < 32u && id < st->cap_prims));
         if (COUNT && rel) s_ids[COUNT ? warp : 0][slot] = id;
         if (rel) {
-            float *e = ef + 12 * (slot >> 1) + (slot & 1);
+            float *e = ef + kPairFloats * (slot >> 1) + (slot & 1);
             if (id >= F) {
                 e[0] = a.x; e[2] = a.y; e[4] = b.x; e[6] = b.z; e[8] = b.y + b.y; e[10] = a.z;
-                wb.col[slot] = make_float4(c.x, c.y, c.z, lg2_ftz(a.w));
+                wb.col(slot) = make_float4(c.x, c.y, c.z, lg2_ftz(a.w));
             } else {
                 // triangle: the staged vertices, kind and alpha; q_max = -1 marks it
                 e[0] = a.x; e[2] = a.y; e[4] = a.z; e[6] = a.w; e[8] = b.x; e[10] = -1.f;
-                wb.col[slot] = make_float4(b.y, b.z, b.w, __uint_as_float(id));
+                wb.col(slot) = make_float4(b.y, b.z, b.w, __uint_as_float(id));
                 const char *src = reinterpret_cast<const char *>(&trec[id].q2);
                 const unsigned dst = (unsigned)__cvta_generic_to_shared(&tat[slot]);
 #pragma unroll
@@ -514,8 +516,8 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
         // zero colour keeps the predicated blend's 0 * colour finite
         const unsigned cnt4 = (cnt + 3) & ~3u;
         if (lane >= cnt && lane < cnt4) {
-            ef[12 * (lane >> 1) + 10 + (lane & 1)] = __int_as_float(0x7fc00000);
-            wb.col[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+            ef[kPairFloats * (lane >> 1) + 10 + (lane & 1)] = __int_as_float(0x7fc00000);
+            wb.col(lane) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         __syncwarp();  // packing done, the stage slot is free again
         stage_rec(id0);  // next chunk's records land while this one is blended
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
                 float al[4];
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
-                    ec[k] = wb.col[2 * p + k];
+                    ec[k] = wb.col(2 * p + k);
                     al[k] = fminf(bp.alpha_max, ex2_ftz(fmaf(q[k], kexp, ec[k].w)));
                 }
                 f32x2 c01 = pk2(s.C0, s.C1);  // (R, G) accumulated as one f32x2 FFMA2
@@ -542,7 +544,17 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
                 for (int k = 0; k < 4; k++) {
                     // (entry 0: a pixel already done has q = NaN, so no T test is needed)
                     const bool h = q[k] <= m[k] && (k == 0 || s.T >= bp.t_eps);
-                    const float w = h ? s.T * al[k] : 0.f;
+                    float w;
+                    if (COUNT || k == 0) {
+                        w = h ? s.T * al[k] : 0.f;
+                    } else {  // h as one predicate (setp ... .and), one select
+                        asm("{\n\t.reg .pred ph, pl;\n\t"
+                            "setp.le.f32 ph, %1, %2;\n\t"
+                            "setp.ge.and.f32 pl, %3, %4, ph;\n\t"
+                            "selp.f32 %0, %5, 0f00000000, pl;\n\t}"
+                            : "=f"(w)
+                            : "f"(q[k]), "f"(m[k]), "f"(s.T), "f"(bp.t_eps), "f"(s.T * al[k]));
+                    }
                     c01 = fma2(pk2(w, w), pk2(ec[k].x, ec[k].y), c01);
                     s.C2 += w * ec[k].z;
                     s.T -= w;  // a fragment closes an open entity: T != Tlast
@@ -584,8 +596,8 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
                         if (q[j] <= m[j] && !s.done()) gblend(q[j], k);
                         continue;
                     }
-                    const float *e = ef + 12 * p + j;
-                    const float4 ec = wb.col[k];
+                    const float *e = ef + kPairFloats * p + j;
+                    const float4 ec = wb.col(k);
                     const int X[3] = {__float_as_int(e[0]), __float_as_int(e[4]), __float_as_int(e[8])};
                     const int Y[3] = {__float_as_int(e[2]), __float_as_int(e[6]), __float_as_int(ec.x)};
                     if (!s.done()) {
@@ -688,7 +700,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_resort(const uint2 *
     const uint2 rg = ranges[tile];
     const unsigned lt = (1u << lane) - 1u;
     WarpBuf &wb = s_buf[warp];
-    float *ef = &wb.e[0][0].x;
+    float *ef = &wb.v[0][0].x;
     TriAttr *tat = s_tri[warp];
     float4 *stg = s_stage[warp][lane];
     const unsigned stg_s = (unsigned)__cvta_generic_to_shared(stg);
@@ -807,14 +819,14 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_resort(const uint2 *
         const unsigned slot = __popc(bal & lt);
         if (rel) {
             s_ids[warp][slot] = id;
-            float *e = ef + 12 * (slot >> 1) + (slot & 1);
+            float *e = ef + kPairFloats * (slot >> 1) + (slot & 1);
             if (id >= F) {
                 e[0] = a.x; e[2] = a.y; e[4] = b.x; e[6] = b.z; e[8] = b.y + b.y; e[10] = a.z;
-                wb.col[slot] = make_float4(c.x, c.y, c.z, lg2_ftz(a.w));
+                wb.col(slot) = make_float4(c.x, c.y, c.z, lg2_ftz(a.w));
                 s_dep[warp][slot] = __uint_as_float(__ldg(dkey + id));
             } else {
                 e[0] = a.x; e[2] = a.y; e[4] = a.z; e[6] = a.w; e[8] = b.x; e[10] = -1.f;
-                wb.col[slot] = make_float4(b.y, b.z, b.w, __uint_as_float(id));
+                wb.col(slot) = make_float4(b.y, b.z, b.w, __uint_as_float(id));
                 const char *src = reinterpret_cast<const char *>(&trec[id].q2);
                 const unsigned dst = (unsigned)__cvta_generic_to_shared(&tat[slot]);
 #pragma unroll
@@ -831,7 +843,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_resort(const uint2 *
         for (unsigned p = 0; 2 * p < cnt; p++) {
             float q[2], m[2];
             {
-                const float4 A = wb.e[p][0], B = wb.e[p][1], Cc = wb.e[p][2];
+                const float4 A = wb.v[p][0], B = wb.v[p][1], Cc = wb.v[p][2];
                 const f32x2 dx = sub2(pk2(px, px), pk2(A.x, A.y));
                 const f32x2 dy = sub2(pk2(s.py, s.py), pk2(A.z, A.w));
                 const f32x2 t = fma2(pk2(B.z, B.w), mul2(dy, dy), mul2(pk2(Cc.x, Cc.y), mul2(dx, dy)));
@@ -846,7 +858,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_resort(const uint2 *
                 if (m[j] >= 0.f) {  // Gaussian entry
                     if (COUNT && !s.done()) w_gt++;
                     if (q[j] <= m[j] && !s.done()) {
-                        const float4 ec = wb.col[k];
+                        const float4 ec = wb.col(k);
                         WinE e;
                         e.a = fminf(bp.alpha_max, ex2_ftz(fmaf(q[j], kexp, ec.w)));
                         e.r = ec.x; e.g = ec.y; e.b = ec.z;
@@ -858,8 +870,8 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend_resort(const uint2 *
                     continue;
                 }
                 if (s.done()) continue;
-                const float *e = ef + 12 * p + j;
-                const float4 ec = wb.col[k];
+                const float *e = ef + kPairFloats * p + j;
+                const float4 ec = wb.col(k);
                 const int X[3] = {__float_as_int(e[0]), __float_as_int(e[4]), __float_as_int(e[8])};
                 const int Y[3] = {__float_as_int(e[2]), __float_as_int(e[6]), __float_as_int(ec.x)};
                 if (COUNT) w_tt++;
