@@ -354,6 +354,7 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
     __shared__ WarpBuf s_buf[NW];
     __shared__ float4 s_stage[NW][32][3];  // this lane's record of the next chunk (cp.async)
     __shared__ TriAttr s_tri[NW][32];      // a packed triangle entry's q2..q5 (cp.async)
+    __shared__ __align__(16) LiveBox s_lb[NW];
     __shared__ int s_next;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -454,24 +455,31 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
         m1 = Cc.w;
     };
 
+    unsigned live_prev = 0;
     for (unsigned base = rg.x; base < rg.y; base += 32) {
-        // the live pixels' bounding box (lane = 8 row + column)
+        // the live pixels' bounding box (lane = 8 row + column), kept in shared memory
+        // and recomputed only when a pixel of the warp has terminated
         const unsigned live = __ballot_sync(0xffffffffu, !s.done());
         if (!live) break;
-        LiveBox lb;
-        {
+        if (live != live_prev) {
+            live_prev = live;
             const unsigned cols = (live | (live >> 8) | (live >> 16) | (live >> 24)) & 0xFFu;
             const int c0 = __ffs(cols) - 1, c1 = 31 - __clz(cols);
             const int r0 = (__ffs(live) - 1) >> 3, r1 = (31 - __clz(live)) >> 3;
-            lb.cx0 = (float)(sx0 + c0) + 0.5f;
-            lb.cx1 = (float)(sx0 + c1) + 0.5f;
-            lb.cy0 = (float)(sy0 + r0) + 0.5f;
-            lb.cy1 = (float)(sy0 + r1) + 0.5f;
-            lb.X0 = 256 * (sx0 + c0);
-            lb.X1 = 256 * (sx0 + c1 + 1) - 1;
-            lb.Y0 = 256 * (sy0 + r0);
-            lb.Y1 = 256 * (sy0 + r1 + 1) - 1;
+            if (lane == 0) {
+                LiveBox &w = s_lb[warp];
+                w.cx0 = (float)(sx0 + c0) + 0.5f;
+                w.cx1 = (float)(sx0 + c1) + 0.5f;
+                w.cy0 = (float)(sy0 + r0) + 0.5f;
+                w.cy1 = (float)(sy0 + r1) + 0.5f;
+                w.X0 = 256 * (sx0 + c0);
+                w.X1 = 256 * (sx0 + c1 + 1) - 1;
+                w.Y0 = 256 * (sy0 + r0);
+                w.Y1 = 256 * (sy0 + r1 + 1) - 1;
+            }
+            __syncwarp();
         }
+        const LiveBox lb = s_lb[warp];
         const unsigned id = id0;
         id0 = id1;
         id1 = base + 64 + lane < rg.y ? __ldg(vals + base + 64 + lane) : 0xFFFFFFFFu;
