@@ -1,7 +1,8 @@
 // blend.cu -- B8: the unified single-pass anti-aliased blend (§3.2).
 //
-// One CTA per 16x16 tile, one pixel per thread, 8 warps that each walk the
-// tile's sorted list (unified ids, (tile, depth, id) order) independently:
+// One warp per 8x4 sub-tile of a 16x16 tile (8 per tile, handed out as work items
+// in runs per CTA), one pixel per lane; each warp walks its tile's sorted list
+// (unified ids, (tile, depth, id) order) independently:
 // records are gathered with 16-byte loads, culled exactly against the warp's
 // 8x4 sub-tile, packed into a per-warp shared buffer and blended in list
 // order; triangle entries are resolved from their 96-byte setup record
@@ -318,8 +319,8 @@ struct WarpBuf {
 };
 constexpr int kPairFloats = 20;  // floats per pair in WarpBuf
 
-// One CTA per 16x16 tile, 8 independent warps, one pixel per lane.  Warp w owns
-// the 8x4 sub-tile (w & 1, w >> 1) and walks the whole tile list in chunks of 32
+// 8 independent warps per CTA, one pixel per lane.  A warp's item (tile, w) is the
+// 8x4 sub-tile (w & 1, w >> 1); it walks the whole tile list in chunks of 32
 // entries (lane l <-> entry 32c + l):
 //   1. the chunk's records (48 B per Gaussian, the first 32 B per triangle) were
 //      copied by cp.async into the warp's stage while the previous chunk was
