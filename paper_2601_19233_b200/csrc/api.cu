@@ -281,6 +281,13 @@ static int make_cam(unimgs_ctx *c, const unimgs_camera *cam, CamParams &cp) {
     memcpy(cp.t, cam->t, sizeof cp.t);
     cp.near_z = cam->near_z;
     cp.far_z = cam->far_z;
+    {   // N4's per-camera clamp limits, in the same IEEE single operations as B1 would
+        // (round-to-nearest mul and div, no contraction possible): bit-identical
+        const float hw = 0.5f * (float)cam->width, hh = 0.5f * (float)cam->height;
+        const float qx = hw / cam->fx, qy = hh / cam->fy;
+        cp.lx = 1.3f * qx;
+        cp.ly = 1.3f * qy;
+    }
     for (int a = 0; a < 3; a++)
         cp.campos[a] = (float)(-((double)cam->R[a] * cam->t[0] + (double)cam->R[3 + a] * cam->t[1] +
                                  (double)cam->R[6 + a] * cam->t[2]));

@@ -58,6 +58,7 @@ struct CamParams {
     float R[9], t[3];
     float near_z, far_z;
     float campos[3];
+    float lx, ly;  // N4 clamp limits 1.3 (W/2) / fx, 1.3 (H/2) / fy (fp32, computed on the host)
 };
 
 // Triangle record, 96 B (6 x 16 B), written by B2 and read by B8:

@@ -159,8 +159,7 @@ __device__ __forceinline__ bool project_gaussian(const GaussInput &gin, int64_t 
 #pragma unroll
             for (int c = 0; c < 3; c++) Sv[3 * a + c] = dot3(A + 3 * a, cam.R + 3 * c);
         // N4
-        const float lx = mul(1.3f, dv(mul(0.5f, (float)cam.W), cam.fx));
-        const float ly = mul(1.3f, dv(mul(0.5f, (float)cam.H), cam.fy));
+        const float lx = cam.lx, ly = cam.ly;  // = mul(1.3, dv(mul(0.5, W), fx)) etc., per camera
         const float tx = mul(fminf(fmaxf(xz, -lx), lx), pv[2]);
         const float ty = mul(fminf(fmaxf(yz, -ly), ly), pv[2]);
         const float zz2 = mul(pv[2], pv[2]);
