@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--prio", type=int, default=1, help="1: preprocess+bin on high-priority streams (0: one stream per context)")
     ap.add_argument("--streams", type=int, default=4,
                     help="renderer contexts on separate CUDA streams; consecutive views overlap")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="views preprocessed together (unimgs_preprocess_multi); --streams must be a multiple")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config single-view numbers (SURVEY §8(d) Reporting; rank 0, N = 1)")
     return ap.parse_args()
@@ -279,7 +281,8 @@ def run_ours(a, rank, world, local_rank):
     # each SM to the other contexts' blends (settings.sort_ctas_per_sm)
     spm = a.sort_ctas_per_sm if a.sort_ctas_per_sm >= 0 else (1 if nS > 1 else 0)
     pool = R.ContextPool(nS, sc.gaussians.count, sc.mesh.num_triangles, 20 << 20, W, H, prio=bool(a.prio),
-                         device=dev, bg=tuple(float(v) for v in sc.bg), sort_mode=a.sort_mode, sort_ctas_per_sm=spm)
+                         device=dev, bg=tuple(float(v) for v in sc.bg), sort_mode=a.sort_mode, sort_ctas_per_sm=spm,
+                         batch=a.batch)
     rs, streams = pool.rs, pool.streams
     r = rs[0]
     ds = R.to_device(sc, dev)
@@ -507,7 +510,7 @@ def run_ours(a, rank, world, local_rank):
                    "gather": ("none" if not gather else "NCCL send/recv to rank 0" if p2p is None else
                               "fused: blend stores into rank 0's buffer over P2P (CUDA IPC)"),
                    "l2": "inputs larger than L2 (scene %.2f GB > 126 MB; per-view K ~7.5M pairs)" % scene_gb,
-                   "parallelism": f"views i mod {world}", "streams_per_gpu": nS,
+                   "parallelism": f"views i mod {world}", "streams_per_gpu": nS, "preprocess_batch": a.batch,
                    "prio_streams": bool(a.prio), "sort_ctas_per_sm": spm},
         "frame_ms": frame_ms,
         "roofline": {"bound": "alu", "kernel": "k_blend", "achieved": achieved, "peak": peak_tops,
