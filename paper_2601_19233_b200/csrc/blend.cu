@@ -336,11 +336,15 @@ constexpr int kPairFloats = 20;  // floats per pair in WarpBuf
 // run each warp takes the next item when it is done with its last (a shared-memory
 // counter), so the warps of a CTA end together and an SM slot is not held by one
 // slow sub-tile while its other warps idle.
-#ifndef UNIMGS_BLEND_MINB
-#define UNIMGS_BLEND_MINB 4
+#ifndef UNIMGS_BLEND_CTA_WARPS
+#define UNIMGS_BLEND_CTA_WARPS 8  // warps per k_blend CTA (any number: the items are (tile, sub-tile))
 #endif
+#ifndef UNIMGS_BLEND_MINB
+#define UNIMGS_BLEND_MINB (32 / UNIMGS_BLEND_CTA_WARPS)  // 64 registers: 32 warps per SM
+#endif
+constexpr int kBlendCtaThreads = 32 * UNIMGS_BLEND_CTA_WARPS, kSubTiles = 8;  // 8 x (8x4) per 16x16 tile
 template <bool COUNT, int MODE, int M>
-__global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(const uint2 *__restrict__ ranges,
+__global__ void __launch_bounds__(kBlendCtaThreads, UNIMGS_BLEND_MINB) k_blend(const uint2 *__restrict__ ranges,
                                                                      const uint32_t *__restrict__ order,
                                                                      const uint32_t *__restrict__ vals,
                                                                      const GaussRecord *__restrict__ grec,
@@ -350,7 +354,7 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
                                                                      BlendParams bp, float4 *__restrict__ out,
                                                                      DevState *st, uint4 *__restrict__ frag_counts) {
     if (st->overflow) return;
-    constexpr int NW = kBlendThreads / 32;  // warps per tile
+    constexpr int NW = UNIMGS_BLEND_CTA_WARPS;  // warps per CTA
     __shared__ unsigned s_ids[COUNT ? NW : 1][32];  // COUNT only: packed entry k's id
     __shared__ WarpBuf s_buf[NW];
     __shared__ float4 s_stage[NW][32][3];  // this lane's record of the next chunk (cp.async)
@@ -376,12 +380,12 @@ __global__ void __launch_bounds__(kBlendThreads, UNIMGS_BLEND_MINB) k_blend(cons
     }
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_items) break;
-    const int sub = (int)(item % NW);
+    const int sub = (int)(item % kSubTiles);
     // COUNT only: per lane (= per pixel) Gaussian / triangle entries tested and fragments
     // blended, and the unified id of the last fragment blended
     unsigned long long w_gt = 0, w_gf = 0, w_tt = 0, w_tf = 0;
     unsigned last_id = 0xFFFFFFFFu;
-    const int tile = (int)__ldg(order + item / NW);  // longest-first schedule (k_tile_order)
+    const int tile = (int)__ldg(order + item / kSubTiles);  // longest-first schedule (k_tile_order)
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int sx0 = tx * kTile + (sub & 1) * 8, sy0 = ty * kTile + (sub >> 1) * 4;
     const int x = sx0 + (lane & 7), y = sy0 + (lane >> 3);
@@ -959,7 +963,7 @@ static int blend_items_per_cta() {
     static const int v = [] {
         const char *e = getenv("UNIMGS_BLEND_ITEMS");
         const int n = e ? atoi(e) : 0;
-        return n >= 1 ? n : 16;
+        return n >= 1 ? n : 2 * UNIMGS_BLEND_CTA_WARPS;
     }();
     return v;
 }
@@ -968,17 +972,17 @@ template <int MODE, int M>
 static void launch_mode(const Buffers &b, const MeshInput &m, const CamParams &cam, const BlendParams &bp, float *out,
                         cudaStream_t s, bool count_work, uint32_t *frag_counts) {
     const int tiles = cam.tiles_x * cam.tiles_y;
-    const unsigned n_items = (unsigned)tiles * (kBlendThreads / 32);
+    const unsigned n_items = (unsigned)tiles * kSubTiles;
     const int per_cta = blend_items_per_cta();
     const unsigned grid = (n_items + per_cta - 1) / per_cta;
     TexView tv{reinterpret_cast<const uchar4 *>(m.tex), m.tw, m.th};
     if (count_work)
-        k_blend<true, MODE, M><<<grid, kBlendThreads, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
+        k_blend<true, MODE, M><<<grid, kBlendCtaThreads, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
                                                                (unsigned)m.F, cam.W, cam.H, cam.tiles_x, n_items,
                                                                per_cta, bp, reinterpret_cast<float4 *>(out), b.st,
                                                                reinterpret_cast<uint4 *>(frag_counts));
     else
-        k_blend<false, MODE, M><<<grid, kBlendThreads, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
+        k_blend<false, MODE, M><<<grid, kBlendCtaThreads, 0, s>>>(b.ranges, b.order, b.sorted_vals, b.grec, b.trec, tv,
                                                                 (unsigned)m.F, cam.W, cam.H, cam.tiles_x, n_items,
                                                                 per_cta, bp, reinterpret_cast<float4 *>(out), b.st,
                                                                 nullptr);
