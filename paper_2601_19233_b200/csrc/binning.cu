@@ -487,6 +487,30 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
             if (s_hd[FULL ? i : 0]) atomicAdd(&st->hist[i / 256][i % 256], s_hd[FULL ? i : 0]);
 }
 
+
+// The lanes of the warp whose digit equals this lane's (the stable multisplit's peer
+// mask; invalid lanes form a group of their own): one ballot per digit bit (4
+// instructions per bit), or one MATCH.ANY -- whose cost grows with the number of
+// distinct digits in the warp, so it is used only for the passes whose digits are
+// nearly uniform across a warp (the depth key's top byte, the tile id's high digit).
+template <int NB, bool MATCH>
+__device__ __forceinline__ unsigned digit_peers(unsigned d, bool valid) {
+    if constexpr (MATCH) {
+        return __match_any_sync(0xffffffffu, valid ? d : 0xFFFFFFFFu);
+    } else {
+        unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int bt = 0; bt < NB; bt++)  // peers &= bit ? ballot : ~ballot
+            asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+                "and.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
+                "vote.sync.ballot.b32 t, p, 0xffffffff;\n\t"
+                "@!p not.b32 t, t;\n\tand.b32 %0, %0, t;\n\t}"
+                : "+r"(peers)
+                : "r"(d), "r"(1u << bt));
+        return peers;
+    }
+}
+
 // ----------------------------------------------------------------------------
 // One stable onesweep LSD pass on `bits` bits at `shift` (Adinets & Merrill).
 // Tiles of 256 x ITEMS keys, warp-striped; warp-level multisplit ranking from
@@ -497,7 +521,7 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
 #ifndef UNIMGS_SORT_MINB
 #define UNIMGS_SORT_MINB 4  // 64 registers: a sort CTA holds a quarter of the SM's register file
 #endif
-template <typename KT, int ITEMS, int NB>
+template <typename KT, int ITEMS, int NB, bool MATCH = false>
 __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MINB)) k_onesweep(const KT *__restrict__ kin,
                                                               const uint32_t *__restrict__ vin, KT *__restrict__ kout,
                                                               uint32_t *__restrict__ vout, const unsigned *n_ptr,
@@ -560,17 +584,7 @@ __global__ void __launch_bounds__(kSortThreads, (ITEMS <= 4 ? 4 : UNIMGS_SORT_MI
             // stable warp multisplit: the lanes holding the same digit
             const bool valid = wbase + 32u * i < n;
             const unsigned d = valid ? (unsigned)((key[i] >> shift) & mask) : 0u;
-            // one ballot per digit bit, NB fixed at compile time (MATCH.ANY costs ~250
-            // SMSP-cycles per warp op on B200, DESIGN.md §5 history)
-            unsigned peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-            for (int bt = 0; bt < NB; bt++)  // peers &= bit ? ballot : ~ballot, 4 instructions per bit
-                asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
-                    "and.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
-                    "vote.sync.ballot.b32 t, p, 0xffffffff;\n\t"
-                    "@!p not.b32 t, t;\n\tand.b32 %0, %0, t;\n\t}"
-                    : "+r"(peers)
-                    : "r"(d), "r"(1u << bt));
+            const unsigned peers = digit_peers<NB, MATCH>(d, valid);
             const unsigned before = valid ? wh[d] : 0u;
             __syncwarp();
             if (valid && (peers & lt) == 0) wh[d] = before + __popc(peers);
@@ -748,7 +762,7 @@ __global__ void __launch_bounds__(256) k_rts_scan(uint32_t *tcnt, uint32_t *gsum
     gsum[(size_t)totals_row * 256 + d] = acc;
 }
 
-template <typename KT, int ITEMS, int NB>
+template <typename KT, int ITEMS, int NB, bool MATCH = false>
 __global__ void __launch_bounds__(kSortThreads, UNIMGS_SORT_MINB) k_downsweep(const KT *__restrict__ kin,
                                                                            const uint32_t *__restrict__ vin,
                                                                            KT *__restrict__ kout,
@@ -810,15 +824,7 @@ __global__ void __launch_bounds__(kSortThreads, UNIMGS_SORT_MINB) k_downsweep(co
     for (int i = 0; i < ITEMS; i++) {
         const bool valid = wbase + 32u * i < n;
         const unsigned d = valid ? (unsigned)((key[i] >> shift) & mask) : 0u;
-        unsigned peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-        for (int bt = 0; bt < NB; bt++)
-            asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
-                "and.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
-                "vote.sync.ballot.b32 t, p, 0xffffffff;\n\t"
-                "@!p not.b32 t, t;\n\tand.b32 %0, %0, t;\n\t}"
-                : "+r"(peers)
-                : "r"(d), "r"(1u << bt));
+        const unsigned peers = digit_peers<NB, MATCH>(d, valid);
         const unsigned before = valid ? wh[d] : 0u;
         __syncwarp();
         if (valid && (peers & lt) == 0) wh[d] = before + __popc(peers);
@@ -941,17 +947,17 @@ static int bits_for(int64_t tiles) {
     return b;
 }
 
-template <typename KT, int ITEMS, int NB>
+template <typename KT, int ITEMS, int NB, bool MATCH = false>
 static void onesweep_launch(DevState *st, unsigned long long *lookback, const KT *kin, const uint32_t *vin, KT *kout,
                             uint32_t *vout, const unsigned *n_ptr, int shift, int hist_row, int slot, int grid,
                             cudaStream_t s) {
     static const bool attr = [] {  // dynamic shared memory above 48 KB, once per instantiation (thread-safe)
-        cudaFuncSetAttribute(k_onesweep<KT, ITEMS, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_onesweep<KT, ITEMS, NB, MATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)onesweep_smem<KT, ITEMS>());
         return true;
     }();
     (void)attr;
-    k_onesweep<KT, ITEMS, NB><<<grid, kSortThreads, onesweep_smem<KT, ITEMS>(), s>>>(
+    k_onesweep<KT, ITEMS, NB, MATCH><<<grid, kSortThreads, onesweep_smem<KT, ITEMS>(), s>>>(
         kin, vin, kout, vout, n_ptr, shift, &st->hist[hist_row][0], slot, lookback, st);
 }
 
@@ -1078,8 +1084,13 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
         const int g1 = sort_grid(P, sm_count, sort_per_sm, kSortThreads * kDepthItems);
         int cur = 0;
         for (int pass = 0; pass < 4; pass++, slot++) {
-            onesweep_pass<uint32_t, kDepthItems>(b, b.pk[cur], b.pv[cur], b.pk[cur ^ 1], b.pv[cur ^ 1], &b.st->n_vis,
-                                                 8 * pass, 8, HIST_DEPTH0 + pass, slot, g1, s);
+            if (pass == 3)  // the exponent byte: few distinct digits per warp
+                onesweep_launch<uint32_t, kDepthItems, 8, true>(b.st, b.lookback, b.pk[cur], b.pv[cur], b.pk[cur ^ 1],
+                                                                b.pv[cur ^ 1], &b.st->n_vis, 24, HIST_DEPTH0 + 3, slot,
+                                                                g1, s);
+            else
+                onesweep_pass<uint32_t, kDepthItems>(b, b.pk[cur], b.pv[cur], b.pk[cur ^ 1], b.pv[cur ^ 1],
+                                                     &b.st->n_vis, 8 * pass, 8, HIST_DEPTH0 + pass, slot, g1, s);
             cur ^= 1;
             launches++;
             mk.mark("depth_onesweep");
@@ -1140,10 +1151,18 @@ int launch_bin(Buffers &b, int64_t P, int64_t N, int64_t F, const CamParams &cam
             k_rts_scan<<<ngroup_max, 256, 0, s>>>(b.tcnt, b.gsum, &b.st->K, ngroup_max, SLOT_RTS0 + pass, b.st);
             mk.mark("rts_scan");
             const size_t smem = onesweep_smem<uint16_t, kSortItems>();
-#define UNIMGS_DS(NB)                                                                                          \
-    k_downsweep<uint16_t, kSortItems, NB><<<g2, kSortThreads, smem, s>>>(kin, b.tv[tc], (uint16_t *)b.tk[tc ^ 1], \
-                                                                      b.tv[tc ^ 1], &b.st->K, sh, b.tcnt, b.gsum, \
-                                                                      ngroup_max, b.st)
+            // the high tile digit (tile rows) is nearly uniform across a warp: MATCH.ANY
+#define UNIMGS_DS(NB)                                                                                             \
+    do {                                                                                                          \
+        if (pass > 0)                                                                                             \
+            k_downsweep<uint16_t, kSortItems, NB, true><<<g2, kSortThreads, smem, s>>>(                           \
+                kin, b.tv[tc], (uint16_t *)b.tk[tc ^ 1], b.tv[tc ^ 1], &b.st->K, sh, b.tcnt, b.gsum, ngroup_max,   \
+                b.st);                                                                                            \
+        else                                                                                                      \
+            k_downsweep<uint16_t, kSortItems, NB><<<g2, kSortThreads, smem, s>>>(                                 \
+                kin, b.tv[tc], (uint16_t *)b.tk[tc ^ 1], b.tv[tc ^ 1], &b.st->K, sh, b.tcnt, b.gsum, ngroup_max,   \
+                b.st);                                                                                            \
+    } while (0)
             UNIMGS_NB_SWITCH(UNIMGS_DS)
 #undef UNIMGS_DS
 #undef UNIMGS_NB_SWITCH
