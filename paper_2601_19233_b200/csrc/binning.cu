@@ -373,11 +373,16 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
     __shared__ unsigned s_hl[256], s_hh[256];
     __shared__ unsigned s_h3[FULL ? 256 : 1];  // mode 1: third tile digit (tile ids >= 65536)
     __shared__ unsigned s_hd[FULL ? 4 * 256 : 1];
+    // s_mark[t]: the last primitive whose first slot lies in (t - 1) PER .. t PER (-1: none);
+    // a prefix max over t gives each thread the primitive holding its first slot
+    __shared__ int s_mark[kScanThreads];
+    __shared__ int s_wm[kScanThreads / 32];
     Key *tk = reinterpret_cast<Key *>(tk_);
     if (st->overflow) return;
     const unsigned K = st->K, n = st->n_vis;
     const unsigned nranges = (K + SLOTS - 1) / SLOTS;
     if (blockIdx.x >= nranges) return;
+    s_mark[threadIdx.x] = -1;
     for (int i = threadIdx.x; i < 256; i += kScanThreads) {
         s_hl[i] = s_hh[i] = 0;
         if (FULL) s_h3[FULL ? i : 0] = 0;
@@ -397,19 +402,36 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
         for (int j = threadIdx.x; j < m; j += kScanThreads) {
             const unsigned i = p0 + j;
             const uint32_t id = ids[i];
-            s_off[j] = (int)(dcnt[i / kScanTile] + prel[i]) - (int)S;
+            const int o = (int)(dcnt[i / kScanTile] + prel[i]) - (int)S;
+            s_off[j] = o;
             s_id[j] = id;
             s_rect[j] = rect[id];
             if (FULL) s_dk[FULL ? j : 0] = dkey[id];
+            const int b = o <= 0 ? 0 : (o + PER - 1) / PER;  // first thread whose first slot is >= o
+            if (b < kScanThreads) atomicMax(&s_mark[b], j);
         }
         if (threadIdx.x == 0) s_off[m] = 0x7FFFFFFF;  // sentinel for the forward walk
         __syncthreads();
+        // e = the largest j < m with s_off[j] <= k0: a block-wide prefix max of the marks
+        int e;
+        {
+            const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+            int v = s_mark[threadIdx.x];
+            s_mark[threadIdx.x] = -1;  // reset for the next range (staged after its first barrier)
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= (unsigned)o) v = max(v, y);
+            }
+            if (lane == 31) s_wm[w] = v;
+            __syncthreads();
+            for (unsigned q = 0; q < w; q++) v = max(v, s_wm[q]);
+            e = v;
+        }
         // thread t expands slots [t * PER, t * PER + PER) of the range
         const int k0 = (int)threadIdx.x * PER;
         if (k0 < (int)ns) {
-            int e = 0;  // largest e < m with s_off[e] <= k0
-            for (int step = 1 << (31 - __clz(m)); step >= 1; step >>= 1)
-                if (e + step < m && s_off[e + step] <= k0) e += step;
+            UNIMGS_CHECK(e >= 0 && e < m && s_off[e] <= k0 && s_off[e + 1] > k0);
             // the first slot's tile by one division, the rest by walking the rectangle
             // row-major (a primitive change lands on its first slot: local 0)
             unsigned x0, x1, tx, ty;
