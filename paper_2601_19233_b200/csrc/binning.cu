@@ -368,8 +368,8 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
     __shared__ uint32_t s_id[MP];
     __shared__ uint2 s_rect[MP];
     __shared__ uint32_t s_dk[FULL ? MP : 1];
-    __shared__ Key s_k[SLOTS];
-    __shared__ uint32_t s_v[SLOTS];
+    __shared__ __align__(16) Key s_k[SLOTS];
+    __shared__ __align__(16) uint32_t s_v[SLOTS];
     __shared__ unsigned s_hl[256], s_hh[256];
     __shared__ unsigned s_h3[FULL ? 256 : 1];  // mode 1: third tile digit (tile ids >= 65536)
     __shared__ unsigned s_hd[FULL ? 4 * 256 : 1];
@@ -485,9 +485,17 @@ __global__ void __launch_bounds__(kScanThreads) k_expand(const uint32_t *__restr
             }
         }
         __syncthreads();
-        for (unsigned k = threadIdx.x; k < ns; k += kScanThreads) {
-            tk[S + k] = s_k[k];
-            tv[S + k] = s_v[k];
+        if (ns == (unsigned)SLOTS) {  // a full range: 16-byte copies (S is a multiple of SLOTS)
+            const uint4 *sk4 = reinterpret_cast<const uint4 *>(s_k), *sv4 = reinterpret_cast<const uint4 *>(s_v);
+            uint4 *tk4 = reinterpret_cast<uint4 *>(tk + S), *tv4 = reinterpret_cast<uint4 *>(tv + S);
+            constexpr int NK4 = SLOTS * (int)sizeof(Key) / 16, NV4 = SLOTS * 4 / 16;
+            for (int i = threadIdx.x; i < NK4; i += kScanThreads) tk4[i] = sk4[i];
+            for (int i = threadIdx.x; i < NV4; i += kScanThreads) tv4[i] = sv4[i];
+        } else {
+            for (unsigned k = threadIdx.x; k < ns; k += kScanThreads) {
+                tk[S + k] = s_k[k];
+                tv[S + k] = s_v[k];
+            }
         }
         if (!FULL)
             for (int i = threadIdx.x; i < 256; i += kScanThreads) tcnt[(size_t)r * 256 + i] = s_hl[i];
