@@ -66,6 +66,30 @@ template <int M>
 __device__ __forceinline__ unsigned coverage(const int X[3], const int Y[3], int x, int y, long long Ec[3]) {
     const int PX = 256 * x + 128, PY = 256 * y + 128;
     unsigned m = (M == 32) ? 0xFFFFFFFFu : ((1u << M) - 1u);
+    // int32 path when the pixel centre is within 64 px of every vertex: |dx|, |dy| < 2^15
+    // and |P - V| < 2^14, so each edge value is below 2^30 and a sample offset below 2^24
+    // -- the same integers as the int64 evaluation below, without its wide multiplies
+    const unsigned near = (unsigned)(abs(PX - X[0]) | abs(PX - X[1]) | abs(PX - X[2]) | abs(PY - Y[0]) |
+                                     abs(PY - Y[1]) | abs(PY - Y[2]));
+    if (near < 16384u) {
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            const int a = (k + 1) % 3, b = (k + 2) % 3;
+            const int dx = X[b] - X[a], dy = Y[b] - Y[a];
+            const int e = dx * (PY - Y[a]) - dy * (PX - X[a]);
+            Ec[k] = e;
+            const int thr = (dy > 0 || (dy == 0 && dx < 0)) ? 0 : 1;
+            unsigned mk = 0;
+#pragma unroll
+            for (int j = 0; j < M; j++) {
+                int ox, oy;
+                sample_offset<M>(j, ox, oy);
+                mk |= (e + 16 * (dx * oy - dy * ox) >= thr ? 1u : 0u) << j;
+            }
+            m &= mk;
+        }
+        return m;
+    }
 #pragma unroll
     for (int k = 0; k < 3; k++) {
         const int a = (k + 1) % 3, b = (k + 2) % 3;
