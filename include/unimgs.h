@@ -16,8 +16,9 @@
  * The pipeline is three calls per view, enqueued on one CUDA stream:
  *   unimgs_preprocess  B1 EWA projection of Gaussians + B2 triangle
  *                      setup with 4-sample coverage (M = 4)
- *   unimgs_bin         per-tile key duplication, onesweep radix sort and
- *                      tile ranges ("incorporate triangle fragments into the
+ *   unimgs_bin         per-tile key duplication, stable radix sorts (onesweep
+ *                      depth passes, reduce-then-scan tile passes) and tile
+ *                      ranges ("incorporate triangle fragments into the
  *                      depth-sorting process")
  *   unimgs_render      B8 unified blend -> out[H][W][4] = (R, G, B, T)
  *
